@@ -1,0 +1,194 @@
+/*
+ * fdwave_cuda.h -- C-ABI of libfdwave_cuda.so, the sm_100a (B200) engine behind
+ * fdwave::Solver<T> (constant-density acoustic propagator of arXiv 2201.05278).
+ *
+ * The reference has no plugin registry: its seam is the Solver<T> class
+ * template, /root/reference/proj/include/fdwave/kernel.hpp:170-495.  Each entry
+ * point below replaces one piece of that class; the reference file:line is given
+ * beside it.  include/fdwave/kernel.hpp (the drop-in C++ header) and
+ * paper_2201_05278_b200/kernel.py (the Python mirror) are thin hosts over this
+ * ABI; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - extern "C", plain pointers and sizes; no exceptions cross the boundary.
+ *  - Every call returns an fdw_status; fdw_last_error(ctx) (or NULL ctx for
+ *    fdw_create failures) gives the message.
+ *  - Scalars of the field type T are passed as void* with desc.dtype_bytes 4
+ *    (float) or 8 (double).
+ *  - Host arrays use the reference padded layout (field.hpp:10-23, grid.hpp:
+ *    37-42): row-major Z,X[,Y], last index fastest, extended grid + halo on each
+ *    side.  For a Z-slab context (world > 1) the host arrays are the LOCAL padded
+ *    slab: global padded Z planes [z_begin, z_end + 2*halo).
+ *  - Flat indices in source/receiver maps are GLOBAL padded flat indices exactly
+ *    as InterpolationMap::Entry::index holds them (acquisition.hpp:79-85).
+ *  - One host thread per context; calls are serialised by the caller
+ *    ("one run per Solver").
+ */
+#ifndef FDWAVE_CUDA_H
+#define FDWAVE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDW_ABI_VERSION 1
+
+typedef enum fdw_status {
+    FDW_OK = 0,
+    FDW_EINVAL = 1,     /* maps to std::invalid_argument */
+    FDW_ECUDA = 2,      /* CUDA runtime error -> std::runtime_error */
+    FDW_ENCCL = 3,      /* NCCL error -> std::runtime_error */
+    FDW_EINSTABLE = 4,  /* non-finite wavefield -> fdwave::instability_error */
+    FDW_ENOMEM = 5,
+    FDW_ESTATE = 6      /* call order violated (e.g. advance before set_medium) */
+} fdw_status;
+
+/* BoundaryCondition, kernel.hpp:27 (same enumerator order). */
+enum { FDW_BC_NULL_DIRICHLET = 0, FDW_BC_NULL_NEUMANN = 1, FDW_BC_NONE = 2 };
+
+/* Stencil kernel variants (fdw_desc.variant). */
+enum {
+    FDW_KERNEL_AUTO = 0,   /* best registered kernel for (ndim, order, dtype) */
+    FDW_KERNEL_SIMPLE = 1, /* one thread per point, cache-fed (parity baseline) */
+    FDW_KERNEL_ZMARCH = 2  /* 3D: 2.5D Z-march, smem X-Y plane + register Z queue */
+};
+
+/* Arithmetic mode (fdw_desc.math). */
+enum {
+    FDW_MATH_EXACT = 0, /* reference association, no FMA contraction: IEEE-identical
+                           to the reference's own x86-64 build (kernel.hpp:398-420) */
+    FDW_MATH_FMA = 1    /* same association, FMA contraction allowed */
+};
+
+/* Advance flags. */
+enum { FDW_ADVANCE_RECORD = 1 /* sample receivers after every step (forward()) */ };
+
+typedef struct fdw_desc {
+    int32_t abi_version;     /* FDW_ABI_VERSION */
+    int32_t ndim;            /* 2 or 3                         grid.hpp:19 */
+    int32_t space_order;     /* even, 2..20                    grid.hpp:26 */
+    int32_t dtype_bytes;     /* 4 (float) or 8 (double)        Solver<T> */
+    uint64_t extended[3];    /* Grid::extended_shape (2D: [2] = 1) grid.hpp:28 */
+    double spacing[3];       /* Grid::spacing                  grid.hpp:21 */
+    double coeffs[11];       /* StencilCoeffs::second, v_0..v_r  stencil.hpp:95 */
+    int32_t bc[3][2];        /* BoundarySpec::face             kernel.hpp:37-45 */
+    double dt;               /* TimeAxis::dt                   time_axis.hpp:18 */
+    uint64_t n_steps;        /* TimeAxis::n_steps (health check at the last step) */
+    uint64_t check_interval; /* kernel.hpp:491 (0 -> 100) */
+    int32_t device;          /* CUDA device ordinal */
+    int32_t variant;         /* FDW_KERNEL_* */
+    int32_t math;            /* FDW_MATH_* */
+    /* Z-slab decomposition (3D only; world == 1 for a single GPU). */
+    int32_t rank;
+    int32_t world;
+    int32_t z_segments;      /* ZMARCH: Z segments per column (0 -> auto) */
+    uint64_t z_begin;        /* first extended Z plane owned by this rank */
+    uint64_t z_end;          /* one past the last owned plane */
+    unsigned char nccl_id[128]; /* ncclUniqueId from fdw_nccl_unique_id (world > 1) */
+} fdw_desc;
+
+typedef struct fdw_solver fdw_solver;
+
+/* Fills *desc with defaults (abi_version, check_interval 100, world 1, AUTO, EXACT). */
+void fdw_desc_init(fdw_desc* desc);
+
+/* Solver<T>::Solver, kernel.hpp:173-186: validates the descriptor and allocates
+ * the device wavefield ring (two levels) and coefficient arrays. */
+fdw_status fdw_create(const fdw_desc* desc, fdw_solver** out);
+fdw_status fdw_destroy(fdw_solver* ctx);
+const char* fdw_last_error(const fdw_solver* ctx);
+const char* fdw_status_string(fdw_status s);
+
+/* Optional: run on a caller stream (cudaStream_t as void*; NULL = own stream). */
+fdw_status fdw_set_stream(fdw_solver* ctx, void* cuda_stream);
+
+/* Solver<T>::precompute, kernel.hpp:276-297: c^2 dt^2 from the velocity in
+ * double (bit-identical to the reference), eta kept as given; the damping
+ * factors (1 - eta dt) and 1/(1 + eta dt) are formed in double inside the
+ * stencil exactly as the reference precomputes them.  Arrays are host (or, with
+ * on_device = 1, device) padded slabs of T. */
+fdw_status fdw_set_medium(fdw_solver* ctx, const void* velocity, const void* eta,
+                          int on_device);
+
+/* Solver<T>::set_sources, kernel.hpp:188-193: CSR view of an InterpolationMap
+ * (offsets[n_points+1], idx/w[offsets[n_points]]) plus the wavelet (double,
+ * >= n_steps + 1 samples when n_points > 0).  Entries outside this rank's slab
+ * are dropped; overlapping windows are merged per index on the host and applied
+ * in the reference's sequential order (kernel.hpp:426-438). */
+fdw_status fdw_set_sources(fdw_solver* ctx, uint64_t n_points, const uint64_t* offsets,
+                           const uint64_t* idx, const double* w, const double* wavelet,
+                           uint64_t n_samples);
+
+/* Solver<T>::set_receivers, kernel.hpp:194-198 (coordinates stay on the host).
+ * Allocates the device seismogram: n_steps + 1 rows of n_points doubles
+ * (per-rank partial sums, acquisition.hpp:150-161). */
+fdw_status fdw_set_receivers(fdw_solver* ctx, uint64_t n_points, const uint64_t* offsets,
+                             const uint64_t* idx, const double* w);
+
+/* current_level()/previous_level() host mirror, kernel.hpp:217-218: upload /
+ * download both levels (local padded slab of T; either pointer may be NULL).
+ * Downloads include the halo exactly as apply_boundary left it. */
+fdw_status fdw_set_levels(fdw_solver* ctx, const void* prev, const void* curr);
+fdw_status fdw_get_levels(fdw_solver* ctx, void* prev, void* curr);
+/* extract_extended, kernel.hpp:313-323: halo-stripped current level (local slab). */
+fdw_status fdw_get_extended(fdw_solver* ctx, void* out);
+
+/* refresh_boundary, kernel.hpp:223 (+ Z-halo exchange between slabs). */
+fdw_status fdw_refresh_boundary(fdw_solver* ctx);
+
+/* record, kernel.hpp:299-304: starts a recording -- seismogram row 0 = the
+ * current level; FDW_ADVANCE_RECORD then writes row (step - step at this call). */
+fdw_status fdw_record(fdw_solver* ctx);
+
+/* n x step(), kernel.hpp:226-233 (sweep -> inject -> swap -> apply_boundary ->
+ * health check when step % check_interval == 0 or step == n_steps), optionally
+ * recording the seismogram row after each step (forward(), kernel.hpp:255-258).
+ * Launched as CUDA-graph chunks; returns FDW_EINSTABLE with *bad_step /
+ * *bad_max (instability_error::step/max_abs) and leaves the state at that step. */
+fdw_status fdw_advance(fdw_solver* ctx, uint64_t n, uint32_t flags, uint64_t* bad_step,
+                       double* bad_max);
+
+/* Device step counter (Solver<T>::step_index, kernel.hpp:219). */
+fdw_status fdw_step_index(fdw_solver* ctx, uint64_t* step);
+/* Resets the step counter (a fresh forward on the same medium). */
+fdw_status fdw_set_step_index(fdw_solver* ctx, uint64_t step);
+
+/* max_abs, kernel.hpp:265-273 over this rank's slab (first non-finite wins). */
+fdw_status fdw_max_abs(fdw_solver* ctx, double* out);
+
+/* Seismogram rows [0, rows) as T (this rank's partial sums cast to T; for
+ * world > 1 use fdw_download_seismogram_f64 and reduce in rank order). */
+fdw_status fdw_download_seismogram(fdw_solver* ctx, void* out, uint64_t rows);
+fdw_status fdw_download_seismogram_f64(fdw_solver* ctx, double* out, uint64_t rows);
+
+/* Waits for all work queued on the context stream. */
+fdw_status fdw_synchronize(fdw_solver* ctx);
+
+/* Profiling: runs n steps with direct launches and CUDA events around every
+ * kernel; ms[k] = mean device ms per launch of kernel class k
+ * (0 sweep, 1 inject, 2 boundary, 3 receivers, 4 health, 5 halo exchange). */
+fdw_status fdw_profile_steps(fdw_solver* ctx, uint64_t n, double ms[6]);
+
+/* Introspection: device layout of one level (elements): row pitch, plane pitch,
+ * column base, stored planes, selected kernel variant. */
+fdw_status fdw_layout(const fdw_solver* ctx, uint64_t* ld, uint64_t* plane,
+                      uint64_t* base, uint64_t* planes, int32_t* variant);
+
+/* ---- host-only helpers (no GPU needed) ---- */
+
+/* Z-slab split of n_ext planes over `world` ranks: [*z_begin, *z_end). */
+fdw_status fdw_slab_range(uint64_t n_ext, int32_t world, int32_t rank, uint64_t* z_begin,
+                          uint64_t* z_end);
+/* Owner rank of global padded flat index (3D slabs; -1 if not an extended point). */
+int32_t fdw_owner_of(uint64_t flat_idx, const uint64_t extended[3], int32_t halo,
+                     int32_t world);
+/* ncclGetUniqueId into out[128]. */
+fdw_status fdw_nccl_unique_id(unsigned char out[128]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDWAVE_CUDA_H */

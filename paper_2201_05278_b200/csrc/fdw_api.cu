@@ -1,0 +1,1096 @@
+// fdw_api.cu -- C-ABI (include/fdwave_cuda.h) over the sm_100a kernels.
+//
+// Host-side restatement of fdwave::Solver<T> (kernel.hpp:170-495) for the
+// device: layout and upload/download of the padded fields, source/receiver
+// index remapping, the step sequence (sweep -> inject -> swap -> boundary ->
+// health) captured as CUDA-graph chunks, and the Z-slab halo exchange over
+// NCCL for multi-GPU runs.  No CPU fallback: every compute path is a kernel.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/fdwave_cuda.h"
+#include "fdw_kernels.cuh"
+
+using fdw::Ctrl;
+using fdw::SweepArgs;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct ProfileSink {
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+};
+
+}  // namespace
+
+struct fdw_solver {
+    fdw_desc d{};
+    std::string err;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 148;
+
+    int ndim = 3, R = 1, tsize = 4;
+    long long P[3] = {1, 1, 1};  // global padded shape
+    long long nzl = 0;           // 3D: owned extended planes; 2D: extended rows (Z)
+    long long nxl = 0, nyl = 0;  // 3D: ext X, ext Y; 2D: ext X (fast), unused
+    long long Lz = 0;            // 3D: stored planes = nzl + 2R; 2D: 1
+    long long rows_alloc = 0;    // rows per stored plane (3D) / total rows (2D)
+    long long ld = 0, plane = 0, base = 0, origin = 0, origin_pad = 0;
+    size_t level_elems = 0;
+
+    void* lvl[2] = {nullptr, nullptr};
+    int cur = 1;  // lvl[cur] is the current level (Solver::curr_)
+    void* c2dt2 = nullptr;
+    void* eta = nullptr;
+    Ctrl* ctrl = nullptr;
+    Ctrl* h_ctrl = nullptr;  // pinned mirror
+    bool medium_set = false;
+
+    int n_tgt = 0;
+    long long* d_tgt = nullptr;
+    unsigned int* d_ent_off = nullptr;
+    double* d_ent_w = nullptr;
+    double* d_wavelet = nullptr;
+    unsigned long long n_wavelet = 0;
+
+    int n_rec = 0;
+    long long* d_rec_idx = nullptr;
+    unsigned int* d_rec_off = nullptr;
+    double* d_rec_w = nullptr;
+    double* d_seis = nullptr;
+    unsigned long long seis_rows = 0;
+
+    unsigned long long host_step = 0;
+    int variant = FDW_KERNEL_SIMPLE;
+    int zseg = 1;
+    int bx = 16;
+
+    std::map<std::tuple<unsigned long long, int, int, int>, cudaGraphExec_t> graphs;
+    ncclComm_t comm = nullptr;
+    ProfileSink* prof = nullptr;
+};
+
+namespace {
+
+fdw_status fail(fdw_solver* c, fdw_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (c)
+        c->err = buf;
+    else
+        g_create_error = buf;
+    return s;
+}
+
+#define CU(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(c, FDW_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                            \
+    } while (0)
+
+#define NC(call)                                                                           \
+    do {                                                                                   \
+        ncclResult_t r_ = (call);                                                          \
+        if (r_ != ncclSuccess)                                                             \
+            return fail(c, FDW_ENCCL, "%s failed: %s", #call, ncclGetErrorString(r_));     \
+    } while (0)
+
+#define CHECK_LAUNCH() CU(cudaGetLastError())
+
+unsigned long long align_up(unsigned long long v, unsigned long long a) { return (v + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------
+// kernel dispatch
+
+template <typename T>
+SweepArgs<T> sweep_args(fdw_solver* c, int src, int dst) {
+    SweepArgs<T> a{};
+    a.u = static_cast<const T*>(c->lvl[src]);
+    a.out = static_cast<T*>(c->lvl[dst]);
+    a.c2dt2 = static_cast<const T*>(c->c2dt2);
+    a.eta = static_cast<const T*>(c->eta);
+    for (int j = 0; j <= c->R; ++j) a.v[j] = static_cast<T>(c->d.coeffs[j]);
+    for (int k = 0; k < 3; ++k) a.ih[k] = T(1);
+    for (int k = 0; k < c->ndim; ++k)
+        a.ih[k] = static_cast<T>(1.0 / (c->d.spacing[k] * c->d.spacing[k]));
+    a.dt = c->d.dt;
+    a.ld = c->ld;
+    a.plane = c->plane;
+    a.origin = c->origin;
+    a.nz = (int)c->nzl;
+    a.nx = (int)c->nxl;
+    a.ny = (int)c->nyl;
+    a.ctrl = c->ctrl;
+    return a;
+}
+
+#define R_SWITCH(R, MACRO) \
+    switch (R) {           \
+        MACRO(1)           \
+        MACRO(2)           \
+        MACRO(3)           \
+        MACRO(4)           \
+        MACRO(5)           \
+        MACRO(6)           \
+        MACRO(7)           \
+        MACRO(8)           \
+        MACRO(9)           \
+        MACRO(10)          \
+        default: break;    \
+    }
+
+template <typename T, bool EX>
+void launch_simple(fdw_solver* c, const SweepArgs<T>& a) {
+    if (c->ndim == 3) {
+        dim3 block(32, 8), grid((unsigned)((a.ny + 31) / 32), (unsigned)((a.nx + 7) / 8), (unsigned)a.nz);
+#define L3(RR) \
+    case RR: fdw::sweep3d_simple<T, RR, EX><<<grid, block, 0, c->stream>>>(a); break;
+        R_SWITCH(c->R, L3)
+#undef L3
+    } else {
+        dim3 block(128, 2), grid((unsigned)((a.nx + 127) / 128), (unsigned)((a.nz + 1) / 2));
+#define L2(RR) \
+    case RR: fdw::sweep2d_simple<T, RR, EX><<<grid, block, 0, c->stream>>>(a); break;
+        R_SWITCH(c->R, L2)
+#undef L2
+    }
+}
+
+template <typename T, int BX>
+dim3 zmarch_grid(const fdw_solver* c) {
+    using S = fdw::ZMarchShape<T, BX>;
+    return dim3((unsigned)((c->nyl + S::TYW - 1) / S::TYW), (unsigned)((c->nxl + BX - 1) / BX),
+                (unsigned)c->zseg);
+}
+
+template <typename T, bool EX>
+bool launch_zmarch(fdw_solver* c, const SweepArgs<T>& a) {
+    constexpr int BX = 16;
+    using S = fdw::ZMarchShape<T, BX>;
+    dim3 block(S::NTY, BX), grid = zmarch_grid<T, BX>(c);
+    switch (c->R) {
+        case 1: fdw::sweep3d_zmarch<T, 1, BX, EX><<<grid, block, 0, c->stream>>>(a); return true;
+        case 2: fdw::sweep3d_zmarch<T, 2, BX, EX><<<grid, block, 0, c->stream>>>(a); return true;
+        case 4: fdw::sweep3d_zmarch<T, 4, BX, EX><<<grid, block, 0, c->stream>>>(a); return true;
+        default: return false;
+    }
+}
+
+bool zmarch_supported(int R) { return R == 1 || R == 2 || R == 4; }
+
+template <typename T>
+int zmarch_occupancy(int R, bool exact) {
+    constexpr int BX = 16;
+    using S = fdw::ZMarchShape<T, BX>;
+    int occ = 0;
+    const void* f = nullptr;
+    if (exact) {
+        f = R == 1 ? (const void*)fdw::sweep3d_zmarch<T, 1, BX, true>
+          : R == 2 ? (const void*)fdw::sweep3d_zmarch<T, 2, BX, true>
+                   : (const void*)fdw::sweep3d_zmarch<T, 4, BX, true>;
+    } else {
+        f = R == 1 ? (const void*)fdw::sweep3d_zmarch<T, 1, BX, false>
+          : R == 2 ? (const void*)fdw::sweep3d_zmarch<T, 2, BX, false>
+                   : (const void*)fdw::sweep3d_zmarch<T, 4, BX, false>;
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, S::THREADS, 0) != cudaSuccess) occ = 1;
+    return occ < 1 ? 1 : occ;
+}
+
+template <typename T>
+fdw_status launch_sweep_t(fdw_solver* c, int src, int dst) {
+    const SweepArgs<T> a = sweep_args<T>(c, src, dst);
+    const bool ex = c->d.math == FDW_MATH_EXACT;
+    if (c->variant == FDW_KERNEL_ZMARCH) {
+        const bool ok = ex ? launch_zmarch<T, true>(c, a) : launch_zmarch<T, false>(c, a);
+        if (!ok) return fail(c, FDW_EINVAL, "zmarch kernel not built for radius %d", c->R);
+    } else {
+        if (ex)
+            launch_simple<T, true>(c, a);
+        else
+            launch_simple<T, false>(c, a);
+    }
+    CHECK_LAUNCH();
+    return FDW_OK;
+}
+
+fdw_status launch_sweep(fdw_solver* c, int src, int dst) {
+    return c->tsize == 4 ? launch_sweep_t<float>(c, src, dst) : launch_sweep_t<double>(c, src, dst);
+}
+
+template <typename T>
+fdw_status launch_inject_t(fdw_solver* c, int dst, int k) {
+    if (c->n_tgt == 0) return FDW_OK;
+    const int tb = 128;
+    fdw::inject_kernel<T, true><<<(c->n_tgt + tb - 1) / tb, tb, 0, c->stream>>>(
+        static_cast<T*>(c->lvl[dst]), static_cast<const T*>(c->c2dt2), static_cast<const T*>(c->eta),
+        c->d.dt, c->d_tgt, c->d_ent_off, c->d_ent_w, c->d_wavelet, c->n_wavelet, c->n_tgt, k, c->ctrl);
+    CHECK_LAUNCH();
+    return FDW_OK;
+}
+
+fdw_status launch_inject(fdw_solver* c, int dst, int k) {
+    return c->tsize == 4 ? launch_inject_t<float>(c, dst, k) : launch_inject_t<double>(c, dst, k);
+}
+
+// apply_boundary (kernel.hpp:67-102) on level `lv`: axis 0, 1, 2 in order.
+// For Z-slabs the Z phase runs only on global faces and the X/Y phases skip
+// the internal ghost planes (those arrive complete from the neighbour).
+template <typename T>
+fdw_status launch_boundary_t(fdw_solver* c, int lv, const Ctrl* ctrl) {
+    T* f = static_cast<T*>(c->lvl[lv]);
+    const int h = c->R;
+    const int tb = 256;
+    auto go = [&](long long origin_pad, long long sa, int n_ext, long long s1, int n1, long long s2,
+                  int n2, int bc_lo, int bc_hi, int do_lo, int do_hi) -> fdw_status {
+        const long long n = (long long)n1 * n2;
+        if (n <= 0 || (!do_lo && !do_hi)) return FDW_OK;
+        fdw::ghost_lines<T><<<(unsigned)((n + tb - 1) / tb), tb, 0, c->stream>>>(
+            f, origin_pad, sa, n_ext, h, s1, n1, s2, n2, bc_lo, bc_hi, do_lo, do_hi, ctrl);
+        CHECK_LAUNCH();
+        return FDW_OK;
+    };
+    fdw_status s;
+    const auto& bc = c->d.bc;
+    if (c->ndim == 3) {
+        const int rank = c->d.rank, world = c->d.world;
+        // axis 0 (Z): lines over all padded (X, Y)
+        s = go(c->origin_pad, c->plane, (int)c->nzl, c->ld, (int)c->P[1], 1, (int)c->P[2], bc[0][0],
+               bc[0][1], rank == 0, rank == world - 1);
+        if (s) return s;
+        const long long p_lo = rank > 0 ? h : 0;
+        const long long p_hi = rank < world - 1 ? c->Lz - h : c->Lz;
+        const long long o = c->origin_pad + p_lo * c->plane;
+        // axis 1 (X): lines over (planes, padded Y)
+        s = go(o, c->ld, (int)c->nxl, c->plane, (int)(p_hi - p_lo), 1, (int)c->P[2], bc[1][0],
+               bc[1][1], 1, 1);
+        if (s) return s;
+        // axis 2 (Y): lines over (planes, padded X)
+        s = go(o, 1, (int)c->nyl, c->plane, (int)(p_hi - p_lo), c->ld, (int)c->P[1], bc[2][0],
+               bc[2][1], 1, 1);
+        if (s) return s;
+    } else {
+        // axis 0 (Z = rows): lines over padded X columns
+        s = go(c->origin_pad, c->ld, (int)c->nzl, 0, 1, 1, (int)c->P[1], bc[0][0], bc[0][1], 1, 1);
+        if (s) return s;
+        // axis 1 (X = fast): lines over padded Z rows
+        s = go(c->origin_pad, 1, (int)c->nxl, c->ld, (int)c->P[0], 0, 1, bc[1][0], bc[1][1], 1, 1);
+        if (s) return s;
+    }
+    return FDW_OK;
+}
+
+fdw_status launch_boundary(fdw_solver* c, int lv, const Ctrl* ctrl) {
+    return c->tsize == 4 ? launch_boundary_t<float>(c, lv, ctrl) : launch_boundary_t<double>(c, lv, ctrl);
+}
+
+ncclDataType_t nccl_type(const fdw_solver* c) { return c->tsize == 4 ? ncclFloat : ncclDouble; }
+
+// Z-halo exchange: R planes per internal face, full padded planes (contiguous).
+fdw_status launch_halo(fdw_solver* c, int lv) {
+    if (c->d.world <= 1 || c->ndim != 3) return FDW_OK;
+    char* f = static_cast<char*>(c->lvl[lv]);
+    const size_t n = (size_t)c->R * c->plane;
+    const size_t bytes_plane = (size_t)c->plane * c->tsize;
+    const int rank = c->d.rank, world = c->d.world;
+    NC(ncclGroupStart());
+    if (rank > 0) {
+        NC(ncclSend(f + (size_t)c->R * bytes_plane, n, nccl_type(c), rank - 1, c->comm, c->stream));
+        NC(ncclRecv(f, n, nccl_type(c), rank - 1, c->comm, c->stream));
+    }
+    if (rank < world - 1) {
+        NC(ncclSend(f + (size_t)(c->Lz - 2 * c->R) * bytes_plane, n, nccl_type(c), rank + 1, c->comm,
+                    c->stream));
+        NC(ncclRecv(f + (size_t)(c->Lz - c->R) * bytes_plane, n, nccl_type(c), rank + 1, c->comm,
+                    c->stream));
+    }
+    NC(ncclGroupEnd());
+    return FDW_OK;
+}
+
+template <typename T>
+fdw_status launch_receivers_t(fdw_solver* c, int lv, int row_add) {
+    if (c->n_rec == 0 || !c->d_seis) return FDW_OK;
+    const int tb = 128;
+    fdw::receivers_kernel<T><<<(c->n_rec + tb - 1) / tb, tb, 0, c->stream>>>(
+        static_cast<const T*>(c->lvl[lv]), c->d_rec_idx, c->d_rec_off, c->d_rec_w, c->d_seis, c->n_rec,
+        c->seis_rows, row_add, c->ctrl);
+    CHECK_LAUNCH();
+    return FDW_OK;
+}
+
+fdw_status launch_receivers(fdw_solver* c, int lv, int row_add) {
+    return c->tsize == 4 ? launch_receivers_t<float>(c, lv, row_add) : launch_receivers_t<double>(c, lv, row_add);
+}
+
+// Health reduction over this rank's owned padded planes (global faces keep
+// their ghost planes; internal ghost planes belong to the neighbour).
+template <typename T>
+fdw_status launch_health_t(fdw_solver* c, int lv, int honor_abort) {
+    fdw::health_reset<<<1, 1, 0, c->stream>>>(c->ctrl, honor_abort);
+    CHECK_LAUNCH();
+    const T* u = static_cast<const T*>(c->lvl[lv]);
+    long long p_lo = 0, p_hi = 1, n_rows, n_cols;
+    unsigned long long gp0 = 0, gp_lo = 0, gp_hi = 0;
+    if (c->ndim == 3) {
+        p_lo = c->d.rank > 0 ? c->R : 0;
+        p_hi = c->d.rank < c->d.world - 1 ? c->Lz - c->R : c->Lz;
+        gp0 = c->d.z_begin + p_lo;  // global padded plane of local plane p_lo
+        gp_lo = c->d.z_begin;       // global padded plane of local plane 0
+        gp_hi = c->d.z_begin + c->Lz;
+        n_rows = c->P[1];
+        n_cols = c->P[2];
+    } else {
+        n_rows = c->P[0];
+        n_cols = c->P[1];
+    }
+    const long long total_rows = (p_hi - p_lo) * n_rows;
+    const int blocks = (int)std::min<long long>(total_rows, (long long)c->sm_count * 8);
+    fdw::health_kernel<T><<<blocks, 256, 0, c->stream>>>(
+        u, c->origin_pad + p_lo * c->plane, c->ld, c->plane, (int)(p_hi - p_lo), (int)n_rows,
+        (int)n_cols, gp0, (unsigned long long)c->P[1], (unsigned long long)c->P[2], c->ndim == 3,
+        c->ctrl, honor_abort);
+    CHECK_LAUNCH();
+    if (c->d.world > 1) {
+        NC(ncclAllReduce(&c->ctrl->bad_idx, &c->ctrl->bad_idx, 1, ncclUint64, ncclMin, c->comm, c->stream));
+        NC(ncclAllReduce(&c->ctrl->max_bits, &c->ctrl->max_bits, 1, ncclUint64, ncclMax, c->comm, c->stream));
+    }
+    fdw::health_classify<T><<<1, 1, 0, c->stream>>>(
+        u, c->ctrl, c->origin_pad, c->ld, c->plane, gp_lo, gp_hi, (unsigned long long)c->P[1],
+        (unsigned long long)c->P[2], c->ndim == 3, honor_abort);
+    CHECK_LAUNCH();
+    if (c->d.world > 1)
+        NC(ncclAllReduce(&c->ctrl->kind, &c->ctrl->kind, 1, ncclUint32, ncclMax, c->comm, c->stream));
+    return FDW_OK;
+}
+
+fdw_status launch_health(fdw_solver* c, int lv, int honor_abort) {
+    return c->tsize == 4 ? launch_health_t<float>(c, lv, honor_abort) : launch_health_t<double>(c, lv, honor_abort);
+}
+
+// -- profiling marks (direct-launch mode only) --
+struct Mark {
+    fdw_solver* c;
+    int cls;
+    cudaEvent_t a = nullptr, b = nullptr;
+    Mark(fdw_solver* c_, int cls_) : c(c_), cls(cls_) {
+        if (c->prof) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    ~Mark() {
+        if (c->prof) {
+            cudaEventRecord(b, c->stream);
+            c->prof->marks.push_back({cls, {a, b}});
+        }
+    }
+};
+
+// One Solver::step (kernel.hpp:226-233) with relative index k inside a chunk;
+// `src` is the current level before the step.
+fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record) {
+    const int dst = 1 - src;
+    fdw_status s;
+    { Mark m(c, 0); if ((s = launch_sweep(c, src, dst))) return s; }
+    { Mark m(c, 1); if ((s = launch_inject(c, dst, k))) return s; }
+    // swap: dst is now the current level
+    { Mark m(c, 2); if ((s = launch_boundary(c, dst, c->ctrl))) return s; }
+    if (c->d.world > 1) { Mark m(c, 5); if ((s = launch_halo(c, dst))) return s; }
+    if (record) { Mark m(c, 3); if ((s = launch_receivers(c, dst, k + 1))) return s; }
+    return FDW_OK;
+}
+
+fdw_status enqueue_chunk(fdw_solver* c, unsigned long long L, int cur0, bool check, bool record) {
+    fdw_status s;
+    for (unsigned long long k = 0; k < L; ++k)
+        if ((s = enqueue_step(c, (int)k, cur0 ^ (int)(k & 1), record))) return s;
+    fdw::step_advance<<<1, 1, 0, c->stream>>>(c->ctrl, L);
+    CHECK_LAUNCH();
+    if (check) {
+        const int lv = cur0 ^ (int)(L & 1);
+        Mark m(c, 4);
+        if ((s = launch_health(c, lv, 1))) return s;
+        fdw::health_latch<<<1, 1, 0, c->stream>>>(c->ctrl);
+        CHECK_LAUNCH();
+    }
+    return FDW_OK;
+}
+
+fdw_status run_chunk(fdw_solver* c, unsigned long long L, bool check, bool record) {
+    const int cur0 = c->cur;
+    if (L < 8 || c->prof) {
+        fdw_status s = enqueue_chunk(c, L, cur0, check, record);
+        if (s) return s;
+    } else {
+        const auto key = std::make_tuple(L, cur0, (int)check, (int)record);
+        auto it = c->graphs.find(key);
+        if (it == c->graphs.end()) {
+            cudaGraph_t g;
+            CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            fdw_status s = enqueue_chunk(c, L, cur0, check, record);
+            cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+            if (s) return s;
+            if (e != cudaSuccess) return fail(c, FDW_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+            cudaGraphExec_t ge;
+            CU(cudaGraphInstantiate(&ge, g, 0));
+            cudaGraphDestroy(g);
+            it = c->graphs.emplace(key, ge).first;
+        }
+        CU(cudaGraphLaunch(it->second, c->stream));
+    }
+    c->cur = cur0 ^ (int)(L & 1);
+    c->host_step += L;
+    return FDW_OK;
+}
+
+fdw_status read_ctrl(fdw_solver* c) {
+    CU(cudaMemcpyAsync(c->h_ctrl, c->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+// Picks the Z-segment count for the Z-march kernel: fill whole waves of
+// resident CTAs while keeping the 2R-plane queue warm-up small.
+int pick_zseg(fdw_solver* c, int occ) {
+    const long long ty = (c->nyl + (64 / (c->tsize / 4)) - 1) / (64 / (c->tsize / 4));
+    const long long tx = (c->nxl + 15) / 16;
+    const long long tiles = ty * tx;
+    const double resident = (double)c->sm_count * occ;
+    double best = -1.0;
+    int best_s = 1;
+    for (int s = 1; s <= 16; ++s) {
+        if (c->nzl / s < 4 * c->R) break;
+        const double ctas = (double)(tiles * s);
+        const double waves = std::ceil(ctas / resident);
+        const double fill = ctas / (waves * resident);
+        const double warm = 1.0 - 0.2 * (2.0 * c->R * s) / (double)c->nzl;
+        const double score = fill * warm;
+        if (score > best + 1e-9) {
+            best = score;
+            best_s = s;
+        }
+    }
+    return best_s;
+}
+
+fdw_status copy_host_to_level(fdw_solver* c, void* dst, const void* src, int on_device) {
+    const size_t row_bytes = (size_t)(c->ndim == 3 ? c->P[2] : c->P[1]) * c->tsize;
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (c->ndim == 3) {
+        const size_t plane_bytes_host = (size_t)c->P[1] * row_bytes;
+        for (long long p = 0; p < c->Lz; ++p)
+            CU(cudaMemcpy2DAsync(static_cast<char*>(dst) + ((size_t)p * c->plane + c->base) * c->tsize,
+                                 (size_t)c->ld * c->tsize,
+                                 static_cast<const char*>(src) + (size_t)p * plane_bytes_host, row_bytes,
+                                 row_bytes, (size_t)c->P[1], kind, c->stream));
+    } else {
+        CU(cudaMemcpy2DAsync(static_cast<char*>(dst) + (size_t)c->base * c->tsize, (size_t)c->ld * c->tsize,
+                             src, row_bytes, row_bytes, (size_t)c->P[0], kind, c->stream));
+    }
+    return FDW_OK;
+}
+
+fdw_status copy_level_to_host(fdw_solver* c, void* dst, const void* src) {
+    const size_t row_bytes = (size_t)(c->ndim == 3 ? c->P[2] : c->P[1]) * c->tsize;
+    if (c->ndim == 3) {
+        const size_t plane_bytes_host = (size_t)c->P[1] * row_bytes;
+        for (long long p = 0; p < c->Lz; ++p)
+            CU(cudaMemcpy2DAsync(static_cast<char*>(dst) + (size_t)p * plane_bytes_host, row_bytes,
+                                 static_cast<const char*>(src) + ((size_t)p * c->plane + c->base) * c->tsize,
+                                 (size_t)c->ld * c->tsize, row_bytes, (size_t)c->P[1],
+                                 cudaMemcpyDeviceToHost, c->stream));
+    } else {
+        CU(cudaMemcpy2DAsync(dst, row_bytes, static_cast<const char*>(src) + (size_t)c->base * c->tsize,
+                             (size_t)c->ld * c->tsize, row_bytes, (size_t)c->P[0], cudaMemcpyDeviceToHost,
+                             c->stream));
+    }
+    return FDW_OK;
+}
+
+// Global padded flat index -> device element offset (-1: not on this rank).
+long long remap(const fdw_solver* c, unsigned long long flat) {
+    if (c->ndim == 3) {
+        const unsigned long long P12 = (unsigned long long)c->P[1] * c->P[2];
+        const unsigned long long gp = flat / P12, rem = flat % P12;
+        if (gp >= (unsigned long long)c->P[0]) return -1;
+        const long long z = (long long)gp - c->R;  // extended Z (may be a ghost)
+        const long long zb = (long long)c->d.z_begin, ze = (long long)c->d.z_end;
+        const bool first = c->d.rank == 0, last = c->d.rank == c->d.world - 1;
+        const bool owned = (z >= zb && z < ze) || (first && z < 0) || (last && z >= ze);
+        if (!owned) return -1;
+        const long long lp = (long long)gp - zb;
+        return c->base + lp * c->plane + (long long)(rem / c->P[2]) * c->ld + (long long)(rem % c->P[2]);
+    }
+    const unsigned long long P1 = (unsigned long long)c->P[1];
+    if (flat >= (unsigned long long)c->P[0] * P1) return -1;
+    return c->base + (long long)(flat / P1) * c->ld + (long long)(flat % P1);
+}
+
+template <typename P>
+fdw_status dev_upload(fdw_solver* c, P** dst, const std::vector<P>& v) {
+    if (*dst) cudaFree(*dst);
+    *dst = nullptr;
+    const size_t n = std::max<size_t>(v.size(), 1);
+    CU(cudaMalloc(dst, n * sizeof(P)));
+    if (!v.empty()) CU(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(P), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status prologue(fdw_solver* c) {
+    if (!c) return FDW_EINVAL;
+    CU(cudaSetDevice(c->d.device));
+    return FDW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void fdw_desc_init(fdw_desc* d) {
+    std::memset(d, 0, sizeof(*d));
+    d->abi_version = FDW_ABI_VERSION;
+    d->ndim = 3;
+    d->space_order = 8;
+    d->dtype_bytes = 4;
+    for (int a = 0; a < 3; ++a) {
+        d->extended[a] = 1;
+        d->spacing[a] = 1.0;
+        d->bc[a][0] = d->bc[a][1] = FDW_BC_NONE;
+    }
+    d->check_interval = 100;
+    d->world = 1;
+    d->variant = FDW_KERNEL_AUTO;
+    d->math = FDW_MATH_EXACT;
+}
+
+const char* fdw_status_string(fdw_status s) {
+    switch (s) {
+        case FDW_OK: return "ok";
+        case FDW_EINVAL: return "invalid argument";
+        case FDW_ECUDA: return "CUDA error";
+        case FDW_ENCCL: return "NCCL error";
+        case FDW_EINSTABLE: return "non-finite wavefield";
+        case FDW_ENOMEM: return "out of memory";
+        case FDW_ESTATE: return "invalid call order";
+    }
+    return "unknown";
+}
+
+const char* fdw_last_error(const fdw_solver* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+fdw_status fdw_slab_range(uint64_t n_ext, int32_t world, int32_t rank, uint64_t* zb, uint64_t* ze) {
+    if (world < 1 || rank < 0 || rank >= world || n_ext < (uint64_t)world) return FDW_EINVAL;
+    // balanced split, larger slabs first (217 over 8 -> 28 x1, 27 x7)
+    *zb = n_ext * (uint64_t)rank / (uint64_t)world;
+    *ze = n_ext * (uint64_t)(rank + 1) / (uint64_t)world;
+    return FDW_OK;
+}
+
+int32_t fdw_owner_of(uint64_t flat, const uint64_t ext[3], int32_t halo, int32_t world) {
+    const uint64_t P1 = ext[1] + 2 * (uint64_t)halo, P2 = ext[2] + 2 * (uint64_t)halo;
+    const long long z = (long long)(flat / (P1 * P2)) - halo;
+    if (z < 0 || z >= (long long)ext[0]) return -1;
+    for (int32_t r = 0; r < world; ++r) {
+        uint64_t b, e;
+        if (fdw_slab_range(ext[0], world, r, &b, &e) == FDW_OK && (uint64_t)z >= b && (uint64_t)z < e) return r;
+    }
+    return -1;
+}
+
+fdw_status fdw_nccl_unique_id(unsigned char out[128]) {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return FDW_ENCCL;
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+    return FDW_OK;
+}
+
+fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
+    fdw_solver* c = nullptr;
+    if (!dp || !out) return fail(nullptr, FDW_EINVAL, "null descriptor");
+    const fdw_desc& d = *dp;
+    if (d.abi_version != FDW_ABI_VERSION) return fail(nullptr, FDW_EINVAL, "ABI version mismatch");
+    if (d.ndim != 2 && d.ndim != 3) return fail(nullptr, FDW_EINVAL, "Field: ndim must be 2 or 3");
+    if (d.space_order < 2 || d.space_order > 20 || d.space_order % 2)
+        return fail(nullptr, FDW_EINVAL, "spatial order must be even and in [2, 20]");
+    if (d.dtype_bytes != 4 && d.dtype_bytes != 8) return fail(nullptr, FDW_EINVAL, "dtype must be 4 or 8 bytes");
+    const int R = d.space_order / 2;
+    for (int a = 0; a < d.ndim; ++a) {
+        if (d.extended[a] < (uint64_t)(2 * R + 2))
+            return fail(nullptr, FDW_EINVAL,
+                        "extended extent %llu on axis %d is below 2*halo+2 = %d (mirror sources would "
+                        "reach the opposite face)",
+                        (unsigned long long)d.extended[a], a, 2 * R + 2);
+        if (!(d.spacing[a] > 0.0)) return fail(nullptr, FDW_EINVAL, "spacing must be positive");
+        for (int s = 0; s < 2; ++s)
+            if (d.bc[a][s] < 0 || d.bc[a][s] > 2) return fail(nullptr, FDW_EINVAL, "bad boundary condition");
+    }
+    if (d.world < 1 || d.rank < 0 || d.rank >= d.world) return fail(nullptr, FDW_EINVAL, "bad rank/world");
+    if (d.world > 1 && d.ndim != 3) return fail(nullptr, FDW_EINVAL, "slab decomposition is 3D only");
+    if (d.world > 1) {
+        if (!(d.z_end > d.z_begin) || d.z_end > d.extended[0] || d.z_end - d.z_begin < (uint64_t)(2 * R))
+            return fail(nullptr, FDW_EINVAL, "slab [%llu, %llu) must own >= %d of %llu planes",
+                        (unsigned long long)d.z_begin, (unsigned long long)d.z_end, 2 * R,
+                        (unsigned long long)d.extended[0]);
+    }
+    if (d.extended[0] > (1u << 30) || d.extended[1] > (1u << 30) || d.extended[2] > (1u << 30))
+        return fail(nullptr, FDW_EINVAL, "extent too large");
+
+    c = new fdw_solver();
+    c->d = d;
+    if (c->d.check_interval == 0) c->d.check_interval = 100;
+    if (c->d.world <= 1) {
+        c->d.world = 1;
+        c->d.rank = 0;
+        c->d.z_begin = 0;
+        c->d.z_end = d.ndim == 3 ? d.extended[0] : d.extended[0];
+    }
+    c->ndim = d.ndim;
+    c->R = R;
+    c->tsize = d.dtype_bytes;
+    for (int a = 0; a < 3; ++a) c->P[a] = (long long)d.extended[a] + (a < d.ndim ? 2 * R : 0);
+    if (d.ndim == 2) c->P[2] = 1;
+
+    const long long EW = 128 / c->tsize;  // elements per 128 bytes
+    const long long slack_cols = 64 + 16, slack_rows = 64;
+    if (c->ndim == 3) {
+        c->nzl = (long long)(c->d.z_end - c->d.z_begin);
+        c->nxl = (long long)d.extended[1];
+        c->nyl = (long long)d.extended[2];
+        c->Lz = c->nzl + 2 * R;
+        c->base = (long long)align_up(R, EW) - R;
+        c->ld = (long long)align_up(c->base + c->P[2] + slack_cols, EW);
+        c->rows_alloc = c->P[1] + slack_rows;
+        c->plane = c->rows_alloc * c->ld;
+        c->origin_pad = c->base;
+        c->origin = c->base + (long long)R * c->plane + (long long)R * c->ld + R;
+        c->level_elems = (size_t)(c->Lz + 1) * c->plane;
+    } else {
+        c->nzl = (long long)d.extended[0];
+        c->nxl = (long long)d.extended[1];
+        c->nyl = 1;
+        c->Lz = 1;
+        c->base = (long long)align_up(R, EW) - R;
+        c->ld = (long long)align_up(c->base + c->P[1] + slack_cols, EW);
+        c->rows_alloc = c->P[0] + slack_rows;
+        c->plane = c->rows_alloc * c->ld;
+        c->origin_pad = c->base;
+        c->origin = c->base + (long long)R * c->ld + R;
+        c->level_elems = (size_t)c->plane;
+    }
+
+    auto bail = [&](fdw_status s) {
+        g_create_error = c->err;
+        fdw_destroy(c);
+        return s;
+    };
+    {
+        cudaError_t e = cudaSetDevice(d.device);
+        if (e != cudaSuccess) {
+            fail(c, FDW_ECUDA, "cudaSetDevice(%d): %s", d.device, cudaGetErrorString(e));
+            return bail(FDW_ECUDA);
+        }
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, d.device) == cudaSuccess) c->sm_count = prop.multiProcessorCount;
+        if (prop.major < 10) {
+            fail(c, FDW_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a", d.device, prop.major,
+                 prop.minor);
+            return bail(FDW_ECUDA);
+        }
+    }
+    auto ck = [&](cudaError_t e, const char* what) -> bool {
+        if (e == cudaSuccess) return true;
+        fail(c, e == cudaErrorMemoryAllocation ? FDW_ENOMEM : FDW_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+        return false;
+    };
+    if (!ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream")) return bail(FDW_ECUDA);
+    c->own_stream = true;
+    const size_t bytes = c->level_elems * c->tsize;
+    for (void** p : {&c->lvl[0], &c->lvl[1], &c->c2dt2, &c->eta}) {
+        if (!ck(cudaMalloc(p, bytes), "cudaMalloc(level)")) return bail(FDW_ENOMEM);
+        if (!ck(cudaMemsetAsync(*p, 0, bytes, c->stream), "memset")) return bail(FDW_ECUDA);
+    }
+    if (!ck(cudaMalloc(&c->ctrl, sizeof(Ctrl)), "cudaMalloc(ctrl)")) return bail(FDW_ENOMEM);
+    if (!ck(cudaMemsetAsync(c->ctrl, 0, sizeof(Ctrl), c->stream), "memset")) return bail(FDW_ECUDA);
+    if (!ck(cudaMallocHost(&c->h_ctrl, sizeof(Ctrl)), "cudaMallocHost")) return bail(FDW_ENOMEM);
+
+    // kernel selection
+    int variant = d.variant;
+    if (variant == FDW_KERNEL_AUTO)
+        variant = (c->ndim == 3 && zmarch_supported(R)) ? FDW_KERNEL_ZMARCH : FDW_KERNEL_SIMPLE;
+    if (variant == FDW_KERNEL_ZMARCH && (c->ndim != 3 || !zmarch_supported(R))) variant = FDW_KERNEL_SIMPLE;
+    c->variant = variant;
+    if (variant == FDW_KERNEL_ZMARCH) {
+        const bool ex = d.math == FDW_MATH_EXACT;
+        const int occ = c->tsize == 4 ? zmarch_occupancy<float>(R, ex) : zmarch_occupancy<double>(R, ex);
+        c->zseg = d.z_segments > 0 ? d.z_segments : pick_zseg(c, occ);
+        if (c->zseg > c->nzl) c->zseg = (int)c->nzl;
+    }
+
+    if (c->d.world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, d.nccl_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&c->comm, c->d.world, id, c->d.rank);
+        if (r != ncclSuccess) {
+            fail(c, FDW_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+            return bail(FDW_ENCCL);
+        }
+    }
+    if (!ck(cudaStreamSynchronize(c->stream), "sync")) return bail(FDW_ECUDA);
+    *out = c;
+    return FDW_OK;
+}
+
+fdw_status fdw_destroy(fdw_solver* c) {
+    if (!c) return FDW_OK;
+    cudaSetDevice(c->d.device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (void* p : {c->lvl[0], c->lvl[1], c->c2dt2, c->eta, (void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off,
+                    (void*)c->d_ent_w, (void*)c->d_wavelet, (void*)c->d_rec_idx, (void*)c->d_rec_off,
+                    (void*)c->d_rec_w, (void*)c->d_seis})
+        if (p) cudaFree(p);
+    if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return FDW_OK;
+}
+
+fdw_status fdw_set_stream(fdw_solver* c, void* stream) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    CU(cudaStreamSynchronize(c->stream));
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    if (stream) {
+        c->stream = static_cast<cudaStream_t>(stream);
+        c->own_stream = false;
+    } else {
+        CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    return FDW_OK;
+}
+
+fdw_status fdw_set_medium(fdw_solver* c, const void* velocity, const void* eta, int on_device) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (!velocity || !eta) return fail(c, FDW_EINVAL, "velocity and eta are required");
+    if ((s = copy_host_to_level(c, c->c2dt2, velocity, on_device))) return s;
+    if ((s = copy_host_to_level(c, c->eta, eta, on_device))) return s;
+    const unsigned long long n = c->level_elems;
+    const int tb = 256;
+    if (c->tsize == 4)
+        fdw::c2dt2_kernel<float><<<(unsigned)((n + tb - 1) / tb), tb, 0, c->stream>>>(static_cast<float*>(c->c2dt2), n, c->d.dt);
+    else
+        fdw::c2dt2_kernel<double><<<(unsigned)((n + tb - 1) / tb), tb, 0, c->stream>>>(static_cast<double*>(c->c2dt2), n, c->d.dt);
+    CHECK_LAUNCH();
+    CU(cudaStreamSynchronize(c->stream));
+    c->medium_set = true;
+    return FDW_OK;
+}
+
+fdw_status fdw_set_sources(fdw_solver* c, uint64_t n_points, const uint64_t* off, const uint64_t* idx,
+                           const double* w, const double* wavelet, uint64_t n_samples) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (n_points > 0 && n_samples < c->d.n_steps + 1)
+        return fail(c, FDW_EINVAL, "wavelet shorter than the time axis");
+    // merge entries per target index, keeping the reference's (point, entry) order
+    std::unordered_map<long long, int> slot;
+    std::vector<long long> tgt;
+    std::vector<std::vector<double>> ws;
+    for (uint64_t p = 0; p < n_points; ++p)
+        for (uint64_t e = off[p]; e < off[p + 1]; ++e) {
+            const long long o = remap(c, idx[e]);
+            if (o < 0) continue;
+            auto it = slot.find(o);
+            if (it == slot.end()) {
+                it = slot.emplace(o, (int)tgt.size()).first;
+                tgt.push_back(o);
+                ws.emplace_back();
+            }
+            ws[it->second].push_back(w[e]);
+        }
+    std::vector<unsigned int> eo(1, 0);
+    std::vector<double> ew;
+    for (auto& v : ws) {
+        ew.insert(ew.end(), v.begin(), v.end());
+        eo.push_back((unsigned int)ew.size());
+    }
+    if ((s = dev_upload(c, &c->d_tgt, tgt))) return s;
+    if ((s = dev_upload(c, &c->d_ent_off, eo))) return s;
+    if ((s = dev_upload(c, &c->d_ent_w, ew))) return s;
+    std::vector<double> wv(wavelet, wavelet + (n_points ? n_samples : 0));
+    if ((s = dev_upload(c, &c->d_wavelet, wv))) return s;
+    c->n_wavelet = wv.size();
+    c->n_tgt = (int)tgt.size();
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    return FDW_OK;
+}
+
+fdw_status fdw_set_receivers(fdw_solver* c, uint64_t n_points, const uint64_t* off, const uint64_t* idx,
+                             const double* w) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    std::vector<long long> ri;
+    std::vector<unsigned int> ro(1, 0);
+    std::vector<double> rw;
+    for (uint64_t p = 0; p < n_points; ++p) {
+        for (uint64_t e = off[p]; e < off[p + 1]; ++e) {
+            const long long o = remap(c, idx[e]);
+            if (o < 0) continue;
+            ri.push_back(o);
+            rw.push_back(w[e]);
+        }
+        ro.push_back((unsigned int)ri.size());
+    }
+    if ((s = dev_upload(c, &c->d_rec_idx, ri))) return s;
+    if ((s = dev_upload(c, &c->d_rec_off, ro))) return s;
+    if ((s = dev_upload(c, &c->d_rec_w, rw))) return s;
+    if (c->d_seis) cudaFree(c->d_seis);
+    c->d_seis = nullptr;
+    c->n_rec = (int)n_points;
+    c->seis_rows = c->d.n_steps + 1;
+    if (n_points) {
+        const size_t bytes = (size_t)c->seis_rows * n_points * sizeof(double);
+        CU(cudaMalloc(&c->d_seis, bytes));
+        CU(cudaMemsetAsync(c->d_seis, 0, bytes, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    return FDW_OK;
+}
+
+fdw_status fdw_set_levels(fdw_solver* c, const void* prev, const void* curr) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (prev && (s = copy_host_to_level(c, c->lvl[1 - c->cur], prev, 0))) return s;
+    if (curr && (s = copy_host_to_level(c, c->lvl[c->cur], curr, 0))) return s;
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status fdw_get_levels(fdw_solver* c, void* prev, void* curr) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (prev && (s = copy_level_to_host(c, prev, c->lvl[1 - c->cur]))) return s;
+    if (curr && (s = copy_level_to_host(c, curr, c->lvl[c->cur]))) return s;
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status fdw_get_extended(fdw_solver* c, void* out) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    const char* src = static_cast<const char*>(c->lvl[c->cur]);
+    const size_t ts = c->tsize;
+    if (c->ndim == 3) {
+        const size_t row = (size_t)c->nyl * ts;
+        for (long long z = 0; z < c->nzl; ++z)
+            CU(cudaMemcpy2DAsync(static_cast<char*>(out) + (size_t)z * c->nxl * row, row,
+                                 src + (size_t)(c->origin + z * c->plane) * ts, (size_t)c->ld * ts, row,
+                                 (size_t)c->nxl, cudaMemcpyDeviceToHost, c->stream));
+    } else {
+        const size_t row = (size_t)c->nxl * ts;
+        CU(cudaMemcpy2DAsync(out, row, src + (size_t)c->origin * ts, (size_t)c->ld * ts, row, (size_t)c->nzl,
+                             cudaMemcpyDeviceToHost, c->stream));
+    }
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status fdw_refresh_boundary(fdw_solver* c) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if ((s = launch_boundary(c, c->cur, nullptr))) return s;
+    if ((s = launch_halo(c, c->cur))) return s;
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status fdw_record(fdw_solver* c) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    unsigned long long base = c->host_step;
+    CU(cudaMemcpyAsync(&c->ctrl->row_base, &base, sizeof(base), cudaMemcpyHostToDevice, c->stream));
+    if ((s = launch_receivers(c, c->cur, 0))) return s;
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status fdw_advance(fdw_solver* c, uint64_t n, uint32_t flags, uint64_t* bad_step, double* bad_max) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (!c->medium_set) return fail(c, FDW_ESTATE, "fdw_set_medium must be called before fdw_advance");
+    const bool record = (flags & FDW_ADVANCE_RECORD) != 0;
+    const unsigned long long ci = c->d.check_interval, total = c->d.n_steps;
+    const unsigned long long start = c->host_step;
+    const int cur_start = c->cur;
+    unsigned long long st = start;
+    const unsigned long long end = start + n;
+    while (st < end) {
+        unsigned long long nxt = (st / ci + 1) * ci;
+        if (total > st) nxt = std::min(nxt, total);
+        const unsigned long long e = std::min(end, nxt);
+        const bool check = (e % ci == 0) || (e == total);
+        if ((s = run_chunk(c, e - st, check, record))) return s;
+        st = e;
+    }
+    if ((s = read_ctrl(c))) return s;
+    if (c->h_ctrl->abort) {
+        // state is frozen at the failing step; restore host bookkeeping
+        c->host_step = c->h_ctrl->step;
+        c->cur = cur_start ^ (int)((c->h_ctrl->step - start) & 1);
+        if (bad_step) *bad_step = c->h_ctrl->bad_step;
+        if (bad_max)
+            *bad_max = c->h_ctrl->kind == 2 ? std::numeric_limits<double>::quiet_NaN()
+                                            : std::numeric_limits<double>::infinity();
+        const unsigned int zero = 0;
+        CU(cudaMemcpyAsync(&c->ctrl->abort, &zero, sizeof(zero), cudaMemcpyHostToDevice, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        return fail(c, FDW_EINSTABLE, "non-finite wavefield at step %llu; timestep is likely unstable",
+                    (unsigned long long)c->h_ctrl->bad_step);
+    }
+    return FDW_OK;
+}
+
+fdw_status fdw_step_index(fdw_solver* c, uint64_t* step) {
+    if (!c || !step) return FDW_EINVAL;
+    *step = c->host_step;
+    return FDW_OK;
+}
+
+fdw_status fdw_set_step_index(fdw_solver* c, uint64_t step) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    unsigned long long v = step;
+    CU(cudaMemcpyAsync(&c->ctrl->step, &v, sizeof(v), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    c->host_step = step;
+    return FDW_OK;
+}
+
+fdw_status fdw_max_abs(fdw_solver* c, double* out) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if ((s = launch_health(c, c->cur, 0))) return s;
+    if ((s = read_ctrl(c))) return s;
+    if (c->h_ctrl->kind == 2)
+        *out = std::numeric_limits<double>::quiet_NaN();
+    else if (c->h_ctrl->kind == 1)
+        *out = std::numeric_limits<double>::infinity();
+    else {
+        double m;
+        std::memcpy(&m, &c->h_ctrl->max_bits, sizeof(m));
+        *out = m;
+    }
+    return FDW_OK;
+}
+
+fdw_status fdw_download_seismogram_f64(fdw_solver* c, double* out, uint64_t rows) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (rows > c->seis_rows) return fail(c, FDW_EINVAL, "rows exceed the seismogram");
+    if (c->n_rec == 0 || rows == 0) return FDW_OK;
+    CU(cudaMemcpyAsync(out, c->d_seis, (size_t)rows * c->n_rec * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status fdw_download_seismogram(fdw_solver* c, void* out, uint64_t rows) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (rows > c->seis_rows) return fail(c, FDW_EINVAL, "rows exceed the seismogram");
+    const size_t n = (size_t)rows * c->n_rec;
+    std::vector<double> tmp(n);
+    if ((s = fdw_download_seismogram_f64(c, tmp.data(), rows))) return s;
+    if (c->tsize == 4) {
+        float* o = static_cast<float*>(out);
+        for (size_t i = 0; i < n; ++i) o[i] = static_cast<float>(tmp[i]);
+    } else {
+        std::memcpy(out, tmp.data(), n * sizeof(double));
+    }
+    return FDW_OK;
+}
+
+fdw_status fdw_synchronize(fdw_solver* c) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status fdw_profile_steps(fdw_solver* c, uint64_t n, double ms[6]) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (!c->medium_set) return fail(c, FDW_ESTATE, "fdw_set_medium must be called first");
+    ProfileSink sink;
+    c->prof = &sink;
+    const unsigned long long ci = c->d.check_interval, total = c->d.n_steps;
+    unsigned long long st = c->host_step;
+    const unsigned long long end = st + n;
+    while (st < end && s == FDW_OK) {
+        unsigned long long nxt = (st / ci + 1) * ci;
+        if (total > st) nxt = std::min(nxt, total);
+        const unsigned long long e = std::min(end, nxt);
+        s = run_chunk(c, e - st, (e % ci == 0) || (e == total), c->n_rec > 0);
+        st = e;
+    }
+    c->prof = nullptr;
+    cudaStreamSynchronize(c->stream);
+    double sum[6] = {0, 0, 0, 0, 0, 0};
+    int cnt[6] = {0, 0, 0, 0, 0, 0};
+    for (auto& m : sink.marks) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, m.second.first, m.second.second);
+        sum[m.first] += t;
+        cnt[m.first] += 1;
+        cudaEventDestroy(m.second.first);
+        cudaEventDestroy(m.second.second);
+    }
+    for (int k = 0; k < 6; ++k) ms[k] = cnt[k] ? sum[k] / cnt[k] : 0.0;
+    if (s) return s;
+    if ((s = read_ctrl(c))) return s;
+    return FDW_OK;
+}
+
+fdw_status fdw_layout(const fdw_solver* c, uint64_t* ld, uint64_t* plane, uint64_t* base, uint64_t* planes,
+                      int32_t* variant) {
+    if (!c) return FDW_EINVAL;
+    if (ld) *ld = (uint64_t)c->ld;
+    if (plane) *plane = (uint64_t)c->plane;
+    if (base) *base = (uint64_t)c->base;
+    if (planes) *planes = (uint64_t)c->Lz;
+    if (variant) *variant = c->variant | (c->zseg << 8);
+    return FDW_OK;
+}
+
+}  // extern "C"

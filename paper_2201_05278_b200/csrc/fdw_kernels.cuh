@@ -1,0 +1,485 @@
+// fdw_kernels.cuh -- sm_100a device code for the constant-density propagator.
+//
+// Every kernel restates one piece of fdwave::Solver<T>
+// (/root/reference/proj/include/fdwave/kernel.hpp); the line range it replaces
+// is in its comment.  Arithmetic follows the reference association exactly.
+// With EXACT = true each operation is an explicitly rounded intrinsic
+// (__fadd_rn/__fmul_rn/...), so no FMA contraction happens and the result is
+// IEEE-identical to the reference's x86-64 build (which has no FMA: no -march,
+// proj/CMakeLists.txt:7-19).  With EXACT = false the compiler may contract.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fdw {
+
+// ---------------------------------------------------------------------------
+// Device control block: step counter, abort latch, health-check scratch.
+struct Ctrl {
+    unsigned long long step;      // Solver::step_ (device authoritative)
+    unsigned long long bad_step;  // step at which the health check tripped
+    unsigned long long bad_idx;   // min global padded flat index of a non-finite value
+    unsigned long long max_bits;  // max |u| over finite values, as double bits
+    unsigned long long row_base;  // seismogram row 0 = this step (set by fdw_record)
+    unsigned int abort;           // latched by the health check; every kernel no-ops
+    unsigned int kind;            // 0 finite, 1 inf, 2 nan (|first non-finite|)
+};
+
+// ---------------------------------------------------------------------------
+template <typename T, bool EXACT>
+struct Ar;
+template <>
+struct Ar<float, true> {
+    static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+    static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+    static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+};
+template <>
+struct Ar<float, false> {
+    static __device__ __forceinline__ float add(float a, float b) { return a + b; }
+    static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
+    static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
+};
+template <>
+struct Ar<double, true> {
+    static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+    static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+    static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+};
+template <>
+struct Ar<double, false> {
+    static __device__ __forceinline__ double add(double a, double b) { return a + b; }
+    static __device__ __forceinline__ double sub(double a, double b) { return a - b; }
+    static __device__ __forceinline__ double mul(double a, double b) { return a * b; }
+};
+
+// 1/(1 + eta dt) and (1 - eta dt) exactly as kernel.hpp:284-287 forms them:
+// double arithmetic on double(eta) * dt, then cast to T.
+template <typename T>
+__device__ __forceinline__ void damping_factors(T eta, double dt, T& om, T& iop) {
+    const double edt = __dmul_rn(static_cast<double>(eta), dt);
+    om = static_cast<T>(__dsub_rn(1.0, edt));
+    iop = static_cast<T>(__ddiv_rn(1.0, __dadd_rn(1.0, edt)));
+}
+
+// kernel.hpp:418-420:  (c2dt2*rhs + 2u - om*prev) * iop.  eta == 0 gives
+// om = iop = 1 exactly, and the multiplications by 1 are identities.
+template <typename T, bool EXACT>
+__device__ __forceinline__ T time_update(T rhs, T uc, T c2, T prev, T eta, double dt) {
+    using A = Ar<T, EXACT>;
+    const T t = A::add(A::mul(c2, rhs), A::mul(T(2), uc));
+    if (eta == T(0)) return A::sub(t, prev);
+    T om, iop;
+    damping_factors(eta, dt, om, iop);
+    return A::mul(A::sub(t, A::mul(om, prev)), iop);
+}
+
+template <typename T>
+struct SweepArgs {
+    const T* __restrict__ u;      // current level
+    T* out;                       // previous level, overwritten with the next one
+    const T* __restrict__ c2dt2;  // c^2 dt^2
+    const T* __restrict__ eta;    // damping eta (1/s)
+    T v[11];                      // v_0..v_r cast to T (kernel.hpp:293)
+    T ih[3];                      // T(1/h^2) per axis (kernel.hpp:290)
+    double dt;
+    long long ld, plane, origin;  // element strides; offset of extended (0,0,0)
+    int nz, nx, ny;               // extended extents (local Z for slabs; 2D: rows nz, cols nx)
+    const Ctrl* ctrl;
+};
+
+// ---------------------------------------------------------------------------
+// sweep_3d<false>, kernel.hpp:381-424 -- one thread per point, cache-fed.
+template <typename T, int R, bool EXACT>
+__global__ void __launch_bounds__(256) sweep3d_simple(SweepArgs<T> a) {
+    using A = Ar<T, EXACT>;
+    if (a.ctrl->abort) return;
+    const int iy = blockIdx.x * 32 + threadIdx.x;
+    const int ix = blockIdx.y * 8 + threadIdx.y;
+    const int iz = blockIdx.z;
+    if (iy >= a.ny || ix >= a.nx) return;
+    const long long i = a.origin + (long long)iz * a.plane + (long long)ix * a.ld + iy;
+    const T* u = a.u;
+    const T uc = __ldg(u + i);
+    T lz = A::mul(a.v[0], uc), lx = A::mul(a.v[0], uc), ly = A::mul(a.v[0], uc);
+#pragma unroll
+    for (int j = 1; j <= R; ++j) {
+        lz = A::add(lz, A::mul(a.v[j], A::add(__ldg(u + i + j * a.plane), __ldg(u + i - j * a.plane))));
+        lx = A::add(lx, A::mul(a.v[j], A::add(__ldg(u + i + j * a.ld), __ldg(u + i - j * a.ld))));
+        ly = A::add(ly, A::mul(a.v[j], A::add(__ldg(u + i + j), __ldg(u + i - j))));
+    }
+    const T rhs = A::add(A::add(A::mul(lz, a.ih[0]), A::mul(lx, a.ih[1])), A::mul(ly, a.ih[2]));
+    a.out[i] = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
+}
+
+// sweep_2d<false>, kernel.hpp:344-379 -- rows are Z, the fast axis is X.
+template <typename T, int R, bool EXACT>
+__global__ void __launch_bounds__(256) sweep2d_simple(SweepArgs<T> a) {
+    using A = Ar<T, EXACT>;
+    if (a.ctrl->abort) return;
+    const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+    const int iz = blockIdx.y * blockDim.y + threadIdx.y;
+    if (ix >= a.nx || iz >= a.nz) return;
+    const long long i = a.origin + (long long)iz * a.ld + ix;
+    const T* u = a.u;
+    const T uc = __ldg(u + i);
+    T lz = A::mul(a.v[0], uc), lx = A::mul(a.v[0], uc);
+#pragma unroll
+    for (int j = 1; j <= R; ++j) {
+        lz = A::add(lz, A::mul(a.v[j], A::add(__ldg(u + i + j * a.ld), __ldg(u + i - j * a.ld))));
+        lx = A::add(lx, A::mul(a.v[j], A::add(__ldg(u + i + j), __ldg(u + i - j))));
+    }
+    const T rhs = A::add(A::mul(lz, a.ih[0]), A::mul(lx, a.ih[1]));
+    a.out[i] = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
+}
+
+// ---------------------------------------------------------------------------
+// 16-byte vectors along the fast (Y) axis.
+template <typename T, int V>
+struct __align__(16) Vec {
+    T e[V];
+};
+
+__device__ __forceinline__ Vec<float, 4> ldg16(const float* p) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    return {{t.x, t.y, t.z, t.w}};
+}
+__device__ __forceinline__ Vec<double, 2> ldg16(const double* p) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    return {{t.x, t.y}};
+}
+// streaming (evict-first) load for data read exactly once per step
+__device__ __forceinline__ Vec<float, 4> ldcs16(const float* p) {
+    const float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+    return {{t.x, t.y, t.z, t.w}};
+}
+__device__ __forceinline__ Vec<double, 2> ldcs16(const double* p) {
+    const double2 t = __ldcs(reinterpret_cast<const double2*>(p));
+    return {{t.x, t.y}};
+}
+__device__ __forceinline__ void st16(float* p, const Vec<float, 4>& v) {
+    *reinterpret_cast<float4*>(p) = make_float4(v.e[0], v.e[1], v.e[2], v.e[3]);
+}
+__device__ __forceinline__ void st16(double* p, const Vec<double, 2>& v) {
+    *reinterpret_cast<double2*>(p) = make_double2(v.e[0], v.e[1]);
+}
+
+template <typename T, int BX>
+struct ZMarchShape {
+    static constexpr int V = 16 / sizeof(T);  // elements per 16-byte vector
+    static constexpr int NTY = 16;            // threads along Y
+    static constexpr int TYW = NTY * V;       // tile width along Y (elements)
+    static constexpr int THREADS = NTY * BX;
+};
+
+// sweep_3d<false>, kernel.hpp:381-424 -- 2.5D blocking.  A CTA owns a BX x TYW
+// column of (X, Y) outputs and marches a Z segment.  The current u plane
+// (tile + radius-R halos in X and Y) is staged in double-buffered shared
+// memory; the Z neighbours of each thread's V outputs live in a register queue
+// of 2R+1 vectors.  Loads for plane z+1 (queue head, halos, prev, c2dt2, eta)
+// are issued before plane z is computed.  One __syncthreads per plane.
+template <typename T, int R, int BX, bool EXACT>
+__global__ void __launch_bounds__(ZMarchShape<T, BX>::THREADS)
+    sweep3d_zmarch(SweepArgs<T> a) {
+    using A = Ar<T, EXACT>;
+    using S = ZMarchShape<T, BX>;
+    constexpr int V = S::V, NTY = S::NTY, TYW = S::TYW;
+    constexpr int HY = ((R + V - 1) / V) * V;  // Y halo, whole vectors
+    constexpr int HYV = HY / V;
+    constexpr int SP = TYW + 2 * HY;           // smem row pitch (elements)
+    constexpr int SR = BX + 2 * R;             // smem rows
+    using VT = Vec<T, V>;
+    __shared__ __align__(16) T sm[2][SR][SP];
+
+    if (a.ctrl->abort) return;
+    const int ty = threadIdx.x, tx = threadIdx.y, tid = tx * NTY + ty;
+    const int ty0 = blockIdx.x * TYW;  // tile origin (extended Y)
+    const int tx0 = blockIdx.y * BX;   // tile origin (extended X)
+    const int y0 = ty0 + ty * V;
+    const int x = tx0 + tx;
+    const int zs = (int)((long long)a.nz * blockIdx.z / gridDim.z);
+    const int ze = (int)((long long)a.nz * (blockIdx.z + 1) / gridDim.z);
+    const long long ld = a.ld, plane = a.plane;
+    const long long col0 = a.origin + (long long)x * ld + y0;
+
+    // X halo: 2R rows x NTY vectors (rows above, then rows below the tile)
+    const bool hx_act = tid < 2 * R * NTY;
+    const int hx_r = tid / NTY, hx_c = tid % NTY;
+    const int hx_gx = hx_r < R ? tx0 - R + hx_r : tx0 + BX + (hx_r - R);
+    const int hx_sr = hx_r < R ? hx_r : BX + R + (hx_r - R);
+    const long long hx_off = a.origin + (long long)hx_gx * ld + ty0 + hx_c * V;
+    // Y halo: BX rows x 2 sides x HYV vectors
+    const bool hy_act = tid < BX * 2 * HYV;
+    const int hy_r = tid / (2 * HYV), hy_k = tid % (2 * HYV);
+    const int hy_side = hy_k / HYV, hy_kv = hy_k % HYV;
+    const int hy_sc = hy_side == 0 ? hy_kv * V : HY + TYW + hy_kv * V;
+    const int hy_gy = hy_side == 0 ? ty0 - HY + hy_kv * V : ty0 + TYW + hy_kv * V;
+    const long long hy_off = a.origin + (long long)(tx0 + hy_r) * ld + hy_gy;
+
+    const T* u = a.u;
+    VT q[2 * R + 1];
+#pragma unroll
+    for (int k = 0; k < 2 * R; ++k) q[k] = ldg16(u + col0 + (long long)(zs - R + k) * plane);
+    VT qn = ldg16(u + col0 + (long long)(zs + R) * plane);
+    VT pv = ldcs16(a.out + col0 + (long long)zs * plane);
+    VT cv = ldcs16(a.c2dt2 + col0 + (long long)zs * plane);
+    VT ev = ldcs16(a.eta + col0 + (long long)zs * plane);
+    VT hxv, hyv;
+    if (hx_act) hxv = ldg16(u + hx_off + (long long)zs * plane);
+    if (hy_act) hyv = ldg16(u + hy_off + (long long)zs * plane);
+
+    const bool xin = x < a.nx;
+    for (int z = zs; z < ze; ++z) {
+        const int b = (z - zs) & 1;
+        *reinterpret_cast<VT*>(&sm[b][R + tx][HY + ty * V]) = q[R];
+        if (hx_act) *reinterpret_cast<VT*>(&sm[b][hx_sr][HY + hx_c * V]) = hxv;
+        if (hy_act) *reinterpret_cast<VT*>(&sm[b][R + hy_r][hy_sc]) = hyv;
+        q[2 * R] = qn;
+        const VT pc = pv, cc = cv, ec = ev;
+        if (z + 1 < ze) {
+            const long long zo = (long long)(z + 1) * plane;
+            qn = ldg16(u + col0 + zo + (long long)R * plane);
+            pv = ldcs16(a.out + col0 + zo);
+            cv = ldcs16(a.c2dt2 + col0 + zo);
+            ev = ldcs16(a.eta + col0 + zo);
+            if (hx_act) hxv = ldg16(u + hx_off + zo);
+            if (hy_act) hyv = ldg16(u + hy_off + zo);
+        }
+        __syncthreads();
+
+        T lz[V], lx[V], ly[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            const T uc = q[R].e[e];
+            lz[e] = A::mul(a.v[0], uc);
+            lx[e] = lz[e];
+            ly[e] = lz[e];
+        }
+        // Y window: smem row R+tx, columns [ty*V, ty*V + 2HY + V)
+        T w[2 * HY + V];
+#pragma unroll
+        for (int k = 0; k < 2 * HYV + 1; ++k) {
+            const VT t = *reinterpret_cast<const VT*>(&sm[b][R + tx][ty * V + k * V]);
+#pragma unroll
+            for (int e = 0; e < V; ++e) w[k * V + e] = t.e[e];
+        }
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+            const VT xp = *reinterpret_cast<const VT*>(&sm[b][R + tx + j][HY + ty * V]);
+            const VT xm = *reinterpret_cast<const VT*>(&sm[b][R + tx - j][HY + ty * V]);
+            const T vj = a.v[j];
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                lz[e] = A::add(lz[e], A::mul(vj, A::add(q[R + j].e[e], q[R - j].e[e])));
+                lx[e] = A::add(lx[e], A::mul(vj, A::add(xp.e[e], xm.e[e])));
+                ly[e] = A::add(ly[e], A::mul(vj, A::add(w[HY + e + j], w[HY + e - j])));
+            }
+        }
+        VT res;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            const T rhs = A::add(A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1])),
+                                 A::mul(ly[e], a.ih[2]));
+            res.e[e] = time_update<T, EXACT>(rhs, q[R].e[e], cc.e[e], pc.e[e], ec.e[e], a.dt);
+        }
+        if (xin) {
+            T* o = a.out + col0 + (long long)z * plane;
+            if (y0 + V <= a.ny) {
+                st16(o, res);
+            } else {
+#pragma unroll
+                for (int e = 0; e < V; ++e)
+                    if (y0 + e < a.ny) o[e] = res.e[e];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 2 * R; ++k) q[k] = q[k + 1];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// inject, kernel.hpp:429-438.  One thread per distinct target index; its
+// entries are applied in the reference's (point, entry) order.
+template <typename T, bool EXACT>
+__global__ void inject_kernel(T* out, const T* __restrict__ c2dt2, const T* __restrict__ eta,
+                              double dt, const long long* __restrict__ tgt,
+                              const unsigned int* __restrict__ ent_off,
+                              const double* __restrict__ ent_w, const double* __restrict__ wavelet,
+                              unsigned long long n_wavelet, int n_tgt, int k, const Ctrl* ctrl) {
+    using A = Ar<T, true>;  // the reference's scalar order; never contracted
+    if (ctrl->abort) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tgt) return;
+    const unsigned long long n = ctrl->step + (unsigned long long)k;
+    if (n >= n_wavelet) return;
+    const double amp = wavelet[n];
+    const long long i = tgt[t];
+    const T c2 = c2dt2[i];
+    const T e = eta[i];
+    T om, iop = T(1);
+    if (e != T(0)) damping_factors(e, dt, om, iop);
+    T val = out[i];
+    for (unsigned int q = ent_off[t]; q < ent_off[t + 1]; ++q)
+        val = A::add(val, A::mul(A::mul(c2, static_cast<T>(__dmul_rn(ent_w[q], amp))), iop));
+    out[i] = val;
+}
+
+// apply_boundary, kernel.hpp:67-102, one axis per launch (the reference's axis
+// order is kept by launching axis 0, 1, 2 in sequence).  One thread per line.
+template <typename T>
+__global__ void ghost_lines(T* f, long long origin_pad, long long sa, int n_ext, int h,
+                            long long s1, int n1, long long s2, int n2, int bc_lo, int bc_hi,
+                            int do_lo, int do_hi, const Ctrl* ctrl) {
+    if (ctrl && ctrl->abort) return;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)n1 * n2) return;
+    const int i2 = (int)(t % n2), i1 = (int)(t / n2);
+    T* line = f + origin_pad + (long long)i1 * s1 + (long long)i2 * s2;
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
+        if (side == 0 ? !do_lo : !do_hi) continue;
+        const int bc = side == 0 ? bc_lo : bc_hi;
+        const long long face = side == 0 ? h : h + n_ext - 1;
+        const long long o = side == 0 ? -1 : 1;
+        T* fp = line + face * sa;
+        if (bc == 0) {  // null Dirichlet
+            *fp = T(0);
+            for (int k = 1; k <= h; ++k) fp[o * k * sa] = -fp[-o * k * sa];
+        } else if (bc == 1) {  // null Neumann
+            for (int k = 1; k <= h; ++k) fp[o * k * sa] = fp[-o * k * sa];
+        } else {
+            for (int k = 1; k <= h; ++k) fp[o * k * sa] = T(0);
+        }
+    }
+}
+
+// record -> sample_receivers, kernel.hpp:299-304 / acquisition.hpp:150-161.
+// One thread per receiver, entries in order, double accumulation without FMA.
+template <typename T>
+__global__ void receivers_kernel(const T* __restrict__ u, const long long* __restrict__ idx,
+                                 const unsigned int* __restrict__ off,
+                                 const double* __restrict__ w, double* seis, int n_rec,
+                                 unsigned long long n_rows, int row_add, const Ctrl* ctrl) {
+    if (ctrl->abort) return;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rec) return;
+    const unsigned long long row = ctrl->step + (unsigned long long)row_add - ctrl->row_base;
+    if (row >= n_rows) return;
+    double acc = 0.0;
+    for (unsigned int e = off[r]; e < off[r + 1]; ++e)
+        acc = __dadd_rn(acc, __dmul_rn(w[e], static_cast<double>(u[idx[e]])));
+    seis[row * (unsigned long long)n_rec + r] = acc;
+}
+
+// max_abs / check_health, kernel.hpp:265-273 and :456-458.  max |u| over
+// finite values plus the smallest global padded flat index holding a
+// non-finite value (the reference returns the first one in flat order).
+template <typename T>
+__global__ void health_kernel(const T* __restrict__ u, long long origin_pad, long long ld,
+                              long long plane, int n_planes, int n_rows, int n_cols,
+                              unsigned long long gplane0, unsigned long long P1,
+                              unsigned long long P2, int is3d, Ctrl* ctrl, int honor_abort) {
+    if (honor_abort && ctrl->abort) return;
+    double m = 0.0;
+    unsigned long long bad = ~0ull;
+    const long long total = (long long)n_planes * n_rows;
+    for (long long pr = blockIdx.x; pr < total; pr += gridDim.x) {
+        const int p = (int)(pr / n_rows), r = (int)(pr % n_rows);
+        const T* row = u + origin_pad + (long long)p * plane + (long long)r * ld;
+        for (int c = threadIdx.x; c < n_cols; c += blockDim.x) {
+            const double av = fabs(static_cast<double>(row[c]));
+            if (!isfinite(av)) {
+                const unsigned long long flat =
+                    is3d ? ((gplane0 + p) * P1 + r) * P2 + c : (unsigned long long)r * P1 + c;
+                bad = flat < bad ? flat : bad;
+            } else {
+                m = av > m ? av : m;
+            }
+        }
+    }
+    // warp then block reduction
+    for (int o = 16; o > 0; o >>= 1) {
+        const double mo = __shfl_down_sync(0xffffffffu, m, o);
+        const unsigned long long bo = __shfl_down_sync(0xffffffffu, bad, o);
+        m = mo > m ? mo : m;
+        bad = bo < bad ? bo : bad;
+    }
+    __shared__ double sm_m[32];
+    __shared__ unsigned long long sm_b[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        sm_m[wid] = m;
+        sm_b[wid] = bad;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        m = lane < nw ? sm_m[lane] : 0.0;
+        bad = lane < nw ? sm_b[lane] : ~0ull;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double mo = __shfl_down_sync(0xffffffffu, m, o);
+            const unsigned long long bo = __shfl_down_sync(0xffffffffu, bad, o);
+            m = mo > m ? mo : m;
+            bad = bo < bad ? bo : bad;
+        }
+        if (lane == 0) {
+            atomicMax(&ctrl->max_bits, (unsigned long long)__double_as_longlong(m));
+            if (bad != ~0ull) atomicMin(&ctrl->bad_idx, bad);
+        }
+    }
+}
+
+__global__ void health_reset(Ctrl* ctrl, int honor_abort) {
+    if (honor_abort && ctrl->abort) return;
+    ctrl->bad_idx = ~0ull;
+    ctrl->max_bits = 0ull;
+    ctrl->kind = 0u;
+}
+
+// Classifies the first non-finite value if this rank owns it (kind 1 inf, 2 nan).
+template <typename T>
+__global__ void health_classify(const T* u, Ctrl* ctrl, long long origin_pad, long long ld,
+                                long long plane, unsigned long long gplane_lo,
+                                unsigned long long gplane_hi, unsigned long long P1,
+                                unsigned long long P2, int is3d, int honor_abort) {
+    if (honor_abort && ctrl->abort) return;
+    const unsigned long long f = ctrl->bad_idx;
+    if (f == ~0ull) return;
+    long long off;
+    if (is3d) {
+        const unsigned long long gp = f / (P1 * P2), rem = f % (P1 * P2);
+        if (gp < gplane_lo || gp >= gplane_hi) return;
+        off = origin_pad + (long long)(gp - gplane_lo) * plane + (long long)(rem / P2) * ld +
+              (long long)(rem % P2);
+    } else {
+        off = origin_pad + (long long)(f / P1) * ld + (long long)(f % P1);
+    }
+    const double av = fabs(static_cast<double>(u[off]));
+    ctrl->kind = isnan(av) ? 2u : 1u;
+}
+
+// Latches the abort flag after a failed check (kernel.hpp:458 throw).
+__global__ void health_latch(Ctrl* ctrl) {
+    if (ctrl->abort) return;
+    if (ctrl->kind != 0u) {
+        ctrl->abort = 1u;
+        ctrl->bad_step = ctrl->step;
+    }
+}
+
+__global__ void step_advance(Ctrl* ctrl, unsigned long long n) {
+    if (!ctrl->abort) ctrl->step += n;
+}
+
+// precompute, kernel.hpp:282-285: c2dt2 = T(c * c * dt * dt) in double, in place
+// over the whole allocation (zero padding stays zero).
+template <typename T>
+__global__ void c2dt2_kernel(T* f, unsigned long long n, double dt) {
+    const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const double cv = static_cast<double>(f[t]);
+    f[t] = static_cast<T>(__dmul_rn(__dmul_rn(__dmul_rn(cv, cv), dt), dt));
+}
+
+}  // namespace fdw
