@@ -133,6 +133,8 @@ fdw_status fdw_set_receivers(fdw_solver* ctx, uint64_t n_points, const uint64_t*
  * Downloads include the halo exactly as apply_boundary left it. */
 fdw_status fdw_set_levels(fdw_solver* ctx, const void* prev, const void* curr);
 fdw_status fdw_get_levels(fdw_solver* ctx, void* prev, void* curr);
+/* Both levels back to the quiescent zero state of a fresh Solver (field.hpp:23). */
+fdw_status fdw_zero_levels(fdw_solver* ctx);
 /* extract_extended, kernel.hpp:313-323: halo-stripped current level (local slab). */
 fdw_status fdw_get_extended(fdw_solver* ctx, void* out);
 
@@ -171,6 +173,9 @@ fdw_status fdw_synchronize(fdw_solver* ctx);
  * kernel; ms[k] = mean device ms per launch of kernel class k
  * (0 sweep, 1 inject, 2 boundary, 3 receivers, 4 health, 5 halo exchange). */
 fdw_status fdw_profile_steps(fdw_solver* ctx, uint64_t n, double ms[6]);
+
+/* Number of kernels this context has launched (CUDA-graph nodes included). */
+fdw_status fdw_launch_count(const fdw_solver* ctx, uint64_t* n);
 
 /* Introspection: device layout of one level (elements): row pitch, plane pitch,
  * column base, stored planes, selected kernel variant. */

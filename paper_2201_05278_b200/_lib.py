@@ -61,6 +61,7 @@ _SIGS = {
     "fdw_set_receivers": (C.c_int, [_P, C.c_uint64, _P, _P, _P]),
     "fdw_set_levels": (C.c_int, [_P, _P, _P]),
     "fdw_get_levels": (C.c_int, [_P, _P, _P]),
+    "fdw_zero_levels": (C.c_int, [_P]),
     "fdw_get_extended": (C.c_int, [_P, _P]),
     "fdw_refresh_boundary": (C.c_int, [_P]),
     "fdw_record": (C.c_int, [_P]),
@@ -72,6 +73,7 @@ _SIGS = {
     "fdw_download_seismogram_f64": (C.c_int, [_P, _P, C.c_uint64]),
     "fdw_synchronize": (C.c_int, [_P]),
     "fdw_profile_steps": (C.c_int, [_P, C.c_uint64, _DP]),
+    "fdw_launch_count": (C.c_int, [_P, _U64P]),
     "fdw_layout": (C.c_int, [_P, _U64P, _U64P, _U64P, _U64P, C.POINTER(C.c_int32)]),
     "fdw_slab_range": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, _U64P, _U64P]),
     "fdw_owner_of": (C.c_int32, [C.c_uint64, _U64P, C.c_int32, C.c_int32]),

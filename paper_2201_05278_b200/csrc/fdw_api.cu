@@ -80,6 +80,10 @@ struct fdw_solver {
     int bx = 16;
 
     std::map<std::tuple<unsigned long long, int, int, int>, cudaGraphExec_t> graphs;
+    std::map<std::tuple<unsigned long long, int, int, int>, unsigned long long> graph_kernels;
+    bool capturing = false;
+    unsigned long long capture_kernels = 0;
+    unsigned long long launches = 0;  // kernels launched (graph nodes included)
     ncclComm_t comm = nullptr;
     ProfileSink* prof = nullptr;
 };
@@ -114,12 +118,50 @@ fdw_status fail(fdw_solver* c, fdw_status s, const char* fmt, ...) {
             return fail(c, FDW_ENCCL, "%s failed: %s", #call, ncclGetErrorString(r_));     \
     } while (0)
 
-#define CHECK_LAUNCH() CU(cudaGetLastError())
+#define CHECK_LAUNCH()                      \
+    do {                                    \
+        CU(cudaGetLastError());             \
+        if (c->capturing)                   \
+            ++c->capture_kernels;           \
+        else                                \
+            ++c->launches;                  \
+    } while (0)
 
 unsigned long long align_up(unsigned long long v, unsigned long long a) { return (v + a - 1) / a * a; }
 
 // ---------------------------------------------------------------------------
 // kernel dispatch
+
+fdw::Faces faces_of(const fdw_solver* c) {
+    fdw::Faces F{};
+    F.nd = c->ndim;
+    if (c->ndim == 3) {
+        F.n[0] = (int)c->nzl;
+        F.n[1] = (int)c->nxl;
+        F.n[2] = (int)c->nyl;
+        F.s[0] = c->plane;
+        F.s[1] = c->ld;
+        F.s[2] = 1;
+    } else {
+        F.n[0] = (int)c->nzl;
+        F.n[1] = (int)c->nxl;
+        F.n[2] = 1;
+        F.s[0] = c->ld;
+        F.s[1] = 1;
+        F.s[2] = 0;
+    }
+    for (int a = 0; a < 3; ++a)
+        for (int sd = 0; sd < 2; ++sd) {
+            const int bc = c->d.bc[a][sd];
+            F.f[a][sd] = bc == FDW_BC_NULL_DIRICHLET ? -1 : bc == FDW_BC_NULL_NEUMANN ? 1 : 0;
+            F.act[a][sd] = a < c->ndim ? 1 : 0;
+        }
+    if (c->ndim == 3) {
+        F.act[0][0] = c->d.rank == 0;
+        F.act[0][1] = c->d.rank == c->d.world - 1;
+    }
+    return F;
+}
 
 template <typename T>
 SweepArgs<T> sweep_args(fdw_solver* c, int src, int dst) {
@@ -139,6 +181,7 @@ SweepArgs<T> sweep_args(fdw_solver* c, int src, int dst) {
     a.nz = (int)c->nzl;
     a.nx = (int)c->nxl;
     a.ny = (int)c->nyl;
+    a.faces = faces_of(c);
     a.ctrl = c->ctrl;
     return a;
 }
@@ -243,7 +286,8 @@ fdw_status launch_inject_t(fdw_solver* c, int dst, int k) {
     const int tb = 128;
     fdw::inject_kernel<T, true><<<(c->n_tgt + tb - 1) / tb, tb, 0, c->stream>>>(
         static_cast<T*>(c->lvl[dst]), static_cast<const T*>(c->c2dt2), static_cast<const T*>(c->eta),
-        c->d.dt, c->d_tgt, c->d_ent_off, c->d_ent_w, c->d_wavelet, c->n_wavelet, c->n_tgt, k, c->ctrl);
+        c->d.dt, c->d_tgt, c->d_ent_off, c->d_ent_w, c->d_wavelet, c->n_wavelet, c->n_tgt, k, c->ctrl,
+        faces_of(c), c->origin, c->R);
     CHECK_LAUNCH();
     return FDW_OK;
 }
@@ -330,8 +374,8 @@ fdw_status launch_halo(fdw_solver* c, int lv) {
 template <typename T>
 fdw_status launch_receivers_t(fdw_solver* c, int lv, int row_add) {
     if (c->n_rec == 0 || !c->d_seis) return FDW_OK;
-    const int tb = 128;
-    fdw::receivers_kernel<T><<<(c->n_rec + tb - 1) / tb, tb, 0, c->stream>>>(
+    fdw::receivers_kernel<T><<<(c->n_rec + fdw::REC_WARPS - 1) / fdw::REC_WARPS, 32 * fdw::REC_WARPS, 0,
+                               c->stream>>>(
         static_cast<const T*>(c->lvl[lv]), c->d_rec_idx, c->d_rec_off, c->d_rec_w, c->d_seis, c->n_rec,
         c->seis_rows, row_add, c->ctrl);
     CHECK_LAUNCH();
@@ -414,8 +458,8 @@ fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record) {
     fdw_status s;
     { Mark m(c, 0); if ((s = launch_sweep(c, src, dst))) return s; }
     { Mark m(c, 1); if ((s = launch_inject(c, dst, k))) return s; }
-    // swap: dst is now the current level
-    { Mark m(c, 2); if ((s = launch_boundary(c, dst, c->ctrl))) return s; }
+    // swap: dst is now the current level; its ghost cells were written by the
+    // sweep and injection kernels (apply_boundary fused, see fdw::Faces)
     if (c->d.world > 1) { Mark m(c, 5); if ((s = launch_halo(c, dst))) return s; }
     if (record) { Mark m(c, 3); if ((s = launch_receivers(c, dst, k + 1))) return s; }
     return FDW_OK;
@@ -448,7 +492,10 @@ fdw_status run_chunk(fdw_solver* c, unsigned long long L, bool check, bool recor
         if (it == c->graphs.end()) {
             cudaGraph_t g;
             CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            c->capturing = true;
+            c->capture_kernels = 0;
             fdw_status s = enqueue_chunk(c, L, cur0, check, record);
+            c->capturing = false;
             cudaError_t e = cudaStreamEndCapture(c->stream, &g);
             if (s) return s;
             if (e != cudaSuccess) return fail(c, FDW_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
@@ -456,8 +503,10 @@ fdw_status run_chunk(fdw_solver* c, unsigned long long L, bool check, bool recor
             CU(cudaGraphInstantiate(&ge, g, 0));
             cudaGraphDestroy(g);
             it = c->graphs.emplace(key, ge).first;
+            c->graph_kernels[key] = c->capture_kernels;
         }
         CU(cudaGraphLaunch(it->second, c->stream));
+        c->launches += c->graph_kernels[key];
     }
     c->cur = cur0 ^ (int)(L & 1);
     c->host_step += L;
@@ -545,6 +594,30 @@ long long remap(const fdw_solver* c, unsigned long long flat) {
     const unsigned long long P1 = (unsigned long long)c->P[1];
     if (flat >= (unsigned long long)c->P[0] * P1) return -1;
     return c->base + (long long)(flat / P1) * c->ld + (long long)(flat % P1);
+}
+
+// Taps that apply_boundary (kernel.hpp:67-102) overwrites in the same step
+// have no effect on the reference's result and are dropped: ghost cells, and
+// points of a null-Dirichlet face (kernel.hpp:87-88).
+bool dropped_target(const fdw_solver* c, unsigned long long flat) {
+    long long p[3] = {0, 0, 0};
+    if (c->ndim == 3) {
+        const unsigned long long P12 = (unsigned long long)c->P[1] * c->P[2];
+        p[0] = (long long)(flat / P12);
+        p[1] = (long long)((flat % P12) / c->P[2]);
+        p[2] = (long long)(flat % c->P[2]);
+    } else {
+        p[0] = (long long)(flat / c->P[1]);
+        p[1] = (long long)(flat % c->P[1]);
+    }
+    for (int a = 0; a < c->ndim; ++a) {
+        const long long e = p[a] - c->R;  // global extended coordinate
+        const long long n = (long long)c->d.extended[a];
+        if (e < 0 || e >= n) return true;
+        if (c->d.bc[a][0] == FDW_BC_NULL_DIRICHLET && e == 0) return true;
+        if (c->d.bc[a][1] == FDW_BC_NULL_DIRICHLET && e == n - 1) return true;
+    }
+    return false;
 }
 
 template <typename P>
@@ -827,7 +900,7 @@ fdw_status fdw_set_sources(fdw_solver* c, uint64_t n_points, const uint64_t* off
     for (uint64_t p = 0; p < n_points; ++p)
         for (uint64_t e = off[p]; e < off[p + 1]; ++e) {
             const long long o = remap(c, idx[e]);
-            if (o < 0) continue;
+            if (o < 0 || dropped_target(c, idx[e])) continue;
             auto it = slot.find(o);
             if (it == slot.end()) {
                 it = slot.emplace(o, (int)tgt.size()).first;
@@ -894,6 +967,15 @@ fdw_status fdw_set_levels(fdw_solver* c, const void* prev, const void* curr) {
     if (prev && (s = copy_host_to_level(c, c->lvl[1 - c->cur], prev, 0))) return s;
     if (curr && (s = copy_host_to_level(c, c->lvl[c->cur], curr, 0))) return s;
     CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status fdw_zero_levels(fdw_solver* c) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    const size_t bytes = c->level_elems * c->tsize;
+    CU(cudaMemsetAsync(c->lvl[0], 0, bytes, c->stream));
+    CU(cudaMemsetAsync(c->lvl[1], 0, bytes, c->stream));
     return FDW_OK;
 }
 
@@ -1079,6 +1161,12 @@ fdw_status fdw_profile_steps(fdw_solver* c, uint64_t n, double ms[6]) {
     for (int k = 0; k < 6; ++k) ms[k] = cnt[k] ? sum[k] / cnt[k] : 0.0;
     if (s) return s;
     if ((s = read_ctrl(c))) return s;
+    return FDW_OK;
+}
+
+fdw_status fdw_launch_count(const fdw_solver* c, uint64_t* n) {
+    if (!c || !n) return FDW_EINVAL;
+    *n = c->launches;
     return FDW_OK;
 }
 

@@ -75,6 +75,72 @@ __device__ __forceinline__ T time_update(T rhs, T uc, T c2, T prev, T eta, doubl
     return A::mul(A::sub(t, A::mul(om, prev)), iop);
 }
 
+// Per-face boundary handling fused into the producers of a level.  After the
+// sweep (and after injection for the injected points) every ghost cell of the
+// new level holds what apply_boundary (kernel.hpp:67-102) would put there:
+// the thread that owns extended point c writes each ghost cell whose mirror
+// source is c (Dirichlet -u, Neumann +u, none 0; corners take the product of
+// the per-axis factors), and Dirichlet face points are forced to +0.  Internal
+// Z faces of a slab are inactive (their ghost planes come from the neighbour).
+struct Faces {
+    int nd;                  // 2 or 3
+    int n[3];                // extended extents (local Z for slabs)
+    long long s[3];          // element strides per axis
+    signed char f[3][2];     // ghost factor per side: -1 Dirichlet, +1 Neumann, 0 none
+    unsigned char act[3][2]; // side is a physical face handled here
+};
+
+__device__ __forceinline__ bool on_dirichlet_face(const Faces& F, const int* c) {
+    bool z = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (a < F.nd) {
+            z |= F.act[a][0] && F.f[a][0] < 0 && c[a] == 0;
+            z |= F.act[a][1] && F.f[a][1] < 0 && c[a] == F.n[a] - 1;
+        }
+    }
+    return z;
+}
+
+__device__ __forceinline__ bool near_face(const Faces& F, const int* c, int R) {
+    bool near = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        if (a < F.nd) near |= (c[a] <= R) || (c[a] >= F.n[a] - 1 - R);
+    return near;
+}
+
+template <typename T>
+__device__ void ghost_writes(T* out, long long i, const int* c, T v, const Faces& F, int R) {
+    long long d[3];
+    int f[3];
+    int m = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (a >= F.nd) continue;
+        const int ca = c[a], na = F.n[a];
+        if (F.act[a][0] && ca >= 1 && ca <= R) {
+            d[m] = -2LL * ca * F.s[a];
+            f[m] = F.f[a][0];
+            ++m;
+        } else if (F.act[a][1] && ca >= na - 1 - R && ca <= na - 2) {
+            d[m] = 2LL * (na - 1 - ca) * F.s[a];
+            f[m] = F.f[a][1];
+            ++m;
+        }
+    }
+    for (int mask = 1; mask < (1 << m); ++mask) {
+        long long dd = 0;
+        int ff = 1;
+        for (int b = 0; b < m; ++b)
+            if (mask & (1 << b)) {
+                dd += d[b];
+                ff *= f[b];
+            }
+        out[i + dd] = ff == 0 ? T(0) : (ff < 0 ? -v : v);
+    }
+}
+
 template <typename T>
 struct SweepArgs {
     const T* __restrict__ u;      // current level
@@ -86,6 +152,7 @@ struct SweepArgs {
     double dt;
     long long ld, plane, origin;  // element strides; offset of extended (0,0,0)
     int nz, nx, ny;               // extended extents (local Z for slabs; 2D: rows nz, cols nx)
+    Faces faces;
     const Ctrl* ctrl;
 };
 
@@ -110,7 +177,13 @@ __global__ void __launch_bounds__(256) sweep3d_simple(SweepArgs<T> a) {
         ly = A::add(ly, A::mul(a.v[j], A::add(__ldg(u + i + j), __ldg(u + i - j))));
     }
     const T rhs = A::add(A::add(A::mul(lz, a.ih[0]), A::mul(lx, a.ih[1])), A::mul(ly, a.ih[2]));
-    a.out[i] = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
+    T res = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
+    const int c[3] = {iz, ix, iy};
+    if (near_face(a.faces, c, R)) {
+        if (on_dirichlet_face(a.faces, c)) res = T(0);
+        ghost_writes(a.out, i, c, res, a.faces, R);
+    }
+    a.out[i] = res;
 }
 
 // sweep_2d<false>, kernel.hpp:344-379 -- rows are Z, the fast axis is X.
@@ -131,7 +204,13 @@ __global__ void __launch_bounds__(256) sweep2d_simple(SweepArgs<T> a) {
         lx = A::add(lx, A::mul(a.v[j], A::add(__ldg(u + i + j), __ldg(u + i - j))));
     }
     const T rhs = A::add(A::mul(lz, a.ih[0]), A::mul(lx, a.ih[1]));
-    a.out[i] = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
+    T res = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
+    const int c[3] = {iz, ix, 0};
+    if (near_face(a.faces, c, R)) {
+        if (on_dirichlet_face(a.faces, c)) res = T(0);
+        ghost_writes(a.out, i, c, res, a.faces, R);
+    }
+    a.out[i] = res;
 }
 
 // ---------------------------------------------------------------------------
@@ -285,6 +364,18 @@ __global__ void __launch_bounds__(ZMarchShape<T, BX>::THREADS)
         }
         if (xin) {
             T* o = a.out + col0 + (long long)z * plane;
+            const int c0[3] = {z, x, y0};
+            const int c1[3] = {z, x, y0 + V - 1};
+            if (near_face(a.faces, c0, R) || near_face(a.faces, c1, R)) {
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    const int c[3] = {z, x, y0 + e};
+                    if (y0 + e < a.ny) {
+                        if (on_dirichlet_face(a.faces, c)) res.e[e] = T(0);
+                        ghost_writes(a.out, col0 + (long long)z * plane + e, c, res.e[e], a.faces, R);
+                    }
+                }
+            }
             if (y0 + V <= a.ny) {
                 st16(o, res);
             } else {
@@ -306,7 +397,8 @@ __global__ void inject_kernel(T* out, const T* __restrict__ c2dt2, const T* __re
                               double dt, const long long* __restrict__ tgt,
                               const unsigned int* __restrict__ ent_off,
                               const double* __restrict__ ent_w, const double* __restrict__ wavelet,
-                              unsigned long long n_wavelet, int n_tgt, int k, const Ctrl* ctrl) {
+                              unsigned long long n_wavelet, int n_tgt, int k, const Ctrl* ctrl,
+                              Faces F, long long origin, int R) {
     using A = Ar<T, true>;  // the reference's scalar order; never contracted
     if (ctrl->abort) return;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -323,6 +415,20 @@ __global__ void inject_kernel(T* out, const T* __restrict__ c2dt2, const T* __re
     for (unsigned int q = ent_off[t]; q < ent_off[t + 1]; ++q)
         val = A::add(val, A::mul(A::mul(c2, static_cast<T>(__dmul_rn(ent_w[q], amp))), iop));
     out[i] = val;
+    // refresh the ghost copies of this point (targets on Dirichlet faces were
+    // dropped on the host: apply_boundary zeroes them after injection)
+    const long long rem = i - origin;
+    int c[3];
+    if (F.nd == 3) {
+        c[0] = (int)(rem / F.s[0]);
+        c[1] = (int)((rem % F.s[0]) / F.s[1]);
+        c[2] = (int)(rem % F.s[1]);
+    } else {
+        c[0] = (int)(rem / F.s[0]);
+        c[1] = (int)(rem % F.s[0]);
+        c[2] = 0;
+    }
+    if (near_face(F, c, R)) ghost_writes(out, i, c, val, F, R);
 }
 
 // apply_boundary, kernel.hpp:67-102, one axis per launch (the reference's axis
@@ -355,21 +461,36 @@ __global__ void ghost_lines(T* f, long long origin_pad, long long sa, int n_ext,
 }
 
 // record -> sample_receivers, kernel.hpp:299-304 / acquisition.hpp:150-161.
-// One thread per receiver, entries in order, double accumulation without FMA.
+// One warp per receiver: the lanes form the products w_e * double(u[idx_e]) in
+// parallel into shared memory, then lane 0 sums them in entry order (double,
+// no FMA) -- the reference's exact association.
+constexpr int REC_WARPS = 4;
+constexpr int REC_CHUNK = 512;
 template <typename T>
-__global__ void receivers_kernel(const T* __restrict__ u, const long long* __restrict__ idx,
-                                 const unsigned int* __restrict__ off,
-                                 const double* __restrict__ w, double* seis, int n_rec,
-                                 unsigned long long n_rows, int row_add, const Ctrl* ctrl) {
+__global__ void __launch_bounds__(32 * REC_WARPS)
+    receivers_kernel(const T* __restrict__ u, const long long* __restrict__ idx,
+                     const unsigned int* __restrict__ off, const double* __restrict__ w, double* seis,
+                     int n_rec, unsigned long long n_rows, int row_add, const Ctrl* ctrl) {
+    __shared__ double prod[REC_WARPS][REC_CHUNK];
     if (ctrl->abort) return;
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_rec) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = blockIdx.x * REC_WARPS + warp;
     const unsigned long long row = ctrl->step + (unsigned long long)row_add - ctrl->row_base;
-    if (row >= n_rows) return;
+    if (r >= n_rec || row >= n_rows) return;
+    const unsigned int b = off[r], e = off[r + 1];
     double acc = 0.0;
-    for (unsigned int e = off[r]; e < off[r + 1]; ++e)
-        acc = __dadd_rn(acc, __dmul_rn(w[e], static_cast<double>(u[idx[e]])));
-    seis[row * (unsigned long long)n_rec + r] = acc;
+    for (unsigned int base = b; base < e; base += REC_CHUNK) {
+        const int m = (int)min((unsigned int)REC_CHUNK, e - base);
+        for (int k = lane; k < m; k += 32)
+            prod[warp][k] = __dmul_rn(w[base + k], static_cast<double>(u[idx[base + k]]));
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll 8
+            for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, prod[warp][k]);
+        }
+        __syncwarp();
+    }
+    if (lane == 0) seis[row * (unsigned long long)n_rec + r] = acc;
 }
 
 // max_abs / check_health, kernel.hpp:265-273 and :456-458.  max |u| over

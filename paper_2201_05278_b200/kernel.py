@@ -400,6 +400,11 @@ class Solver:
         """n device steps without host-mirror traffic (for timing loops)."""
         self._advance(n, FDW_ADVANCE_RECORD if record else 0)
 
+    def reset_state(self):
+        """Quiescent restart on the same medium: zero levels, step 0."""
+        _check(self._ctx, _lib.lib().fdw_zero_levels(self._ctx), "fdw_zero_levels")
+        self.set_step_index(0)
+
     def set_step_index(self, step: int):
         _check(self._ctx, _lib.lib().fdw_set_step_index(self._ctx, step), "fdw_set_step_index")
 
@@ -407,6 +412,11 @@ class Solver:
         ms = (C.c_double * 6)()
         _check(self._ctx, _lib.lib().fdw_profile_steps(self._ctx, n, ms), "fdw_profile_steps")
         return list(ms)
+
+    def launch_count(self) -> int:
+        v = C.c_uint64()
+        _lib.lib().fdw_launch_count(self._ctx, C.byref(v))
+        return int(v.value)
 
     @property
     def ctx(self):
