@@ -53,7 +53,8 @@ enum { FDW_BC_NULL_DIRICHLET = 0, FDW_BC_NULL_NEUMANN = 1, FDW_BC_NONE = 2 };
 enum {
     FDW_KERNEL_AUTO = 0,   /* best registered kernel for (ndim, order, dtype) */
     FDW_KERNEL_SIMPLE = 1, /* one thread per point, cache-fed (parity baseline) */
-    FDW_KERNEL_ZMARCH = 2  /* 3D: 2.5D Z-march, smem X-Y plane + register Z queue */
+    FDW_KERNEL_ZMARCH = 2, /* 3D: 2.5D Z-march, smem X-Y plane + register Z queue (LDG-fed) */
+    FDW_KERNEL_TMA = 3     /* 3D: Z-march fed by cp.async.bulk.tensor (TMA) + mbarrier rings */
 };
 
 /* Arithmetic mode (fdw_desc.math). */
@@ -178,7 +179,8 @@ fdw_status fdw_profile_steps(fdw_solver* ctx, uint64_t n, double ms[6]);
 fdw_status fdw_launch_count(const fdw_solver* ctx, uint64_t* n);
 
 /* Introspection: device layout of one level (elements): row pitch, plane pitch,
- * column base, stored planes, selected kernel variant. */
+ * column base, stored planes, selected kernel variant | z_segments << 8 |
+ * resident CTAs per SM << 16. */
 fdw_status fdw_layout(const fdw_solver* ctx, uint64_t* ld, uint64_t* plane,
                       uint64_t* base, uint64_t* planes, int32_t* variant);
 

@@ -5,6 +5,8 @@
 // index remapping, the step sequence (sweep -> inject -> swap -> boundary ->
 // health) captured as CUDA-graph chunks, and the Z-slab halo exchange over
 // NCCL for multi-GPU runs.  No CPU fallback: every compute path is a kernel.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -12,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -54,6 +57,10 @@ struct fdw_solver {
 
     void* lvl[2] = {nullptr, nullptr};
     int cur = 1;  // lvl[cur] is the current level (Solver::curr_)
+    // ghost-cell state per level: 0 stored & consistent with the boundary
+    // conditions, 1 virtual (stored ghosts stale; the TMA kernel mirrors on
+    // the fly), 2 raw (uploaded by the caller; stored ghosts authoritative)
+    int gstate[2] = {0, 0};
     void* c2dt2 = nullptr;
     void* eta = nullptr;
     Ctrl* ctrl = nullptr;
@@ -78,6 +85,8 @@ struct fdw_solver {
     int variant = FDW_KERNEL_SIMPLE;
     int zseg = 1;
     int bx = 16;
+    int occupancy = 0;
+    int tma_minb = 3;
 
     std::map<std::tuple<unsigned long long, int, int, int>, cudaGraphExec_t> graphs;
     std::map<std::tuple<unsigned long long, int, int, int>, unsigned long long> graph_kernels;
@@ -86,6 +95,9 @@ struct fdw_solver {
     unsigned long long launches = 0;  // kernels launched (graph nodes included)
     ncclComm_t comm = nullptr;
     ProfileSink* prof = nullptr;
+    // TMA descriptors (variant FDW_KERNEL_TMA): u-tile box for each level, and
+    // the prev/c2dt2/eta tile box for each level, c2dt2 and eta
+    CUtensorMap tm_u[2], tm_p[2], tm_c, tm_e;
 };
 
 namespace {
@@ -132,35 +144,85 @@ unsigned long long align_up(unsigned long long v, unsigned long long a) { return
 // ---------------------------------------------------------------------------
 // kernel dispatch
 
-fdw::Faces faces_of(const fdw_solver* c) {
-    fdw::Faces F{};
-    F.nd = c->ndim;
+// Region table for fdw::boundary_kernel: ghost shells (global Z faces only
+// for slabs) and the nodes of active null-Dirichlet faces.
+fdw::BoundaryArgs boundary_args(const fdw_solver* c) {
+    fdw::BoundaryArgs b{};
+    const int h = c->R;
+    b.nd = c->ndim;
+    b.h = h;
+    b.origin_pad = c->origin_pad;
+    const bool lo_z = c->d.rank == 0, hi_z = c->d.rank == c->d.world - 1;
+    int ext[3], P[3];
     if (c->ndim == 3) {
-        F.n[0] = (int)c->nzl;
-        F.n[1] = (int)c->nxl;
-        F.n[2] = (int)c->nyl;
-        F.s[0] = c->plane;
-        F.s[1] = c->ld;
-        F.s[2] = 1;
+        ext[0] = (int)c->nzl; ext[1] = (int)c->nxl; ext[2] = (int)c->nyl;
+        P[0] = (int)c->Lz; P[1] = (int)c->P[1]; P[2] = (int)c->P[2];
+        b.s[0] = c->plane; b.s[1] = c->ld; b.s[2] = 1;
     } else {
-        F.n[0] = (int)c->nzl;
-        F.n[1] = (int)c->nxl;
-        F.n[2] = 1;
-        F.s[0] = c->ld;
-        F.s[1] = 1;
-        F.s[2] = 0;
+        ext[0] = (int)c->nzl; ext[1] = (int)c->nxl; ext[2] = 1;
+        P[0] = (int)c->P[0]; P[1] = (int)c->P[1]; P[2] = 1;
+        b.s[0] = c->ld; b.s[1] = 1; b.s[2] = 0;
     }
-    for (int a = 0; a < 3; ++a)
+    for (int a = 0; a < 3; ++a) {
+        b.ext[a] = ext[a];
         for (int sd = 0; sd < 2; ++sd) {
             const int bc = c->d.bc[a][sd];
-            F.f[a][sd] = bc == FDW_BC_NULL_DIRICHLET ? -1 : bc == FDW_BC_NULL_NEUMANN ? 1 : 0;
-            F.act[a][sd] = a < c->ndim ? 1 : 0;
+            b.f[a][sd] = bc == FDW_BC_NULL_DIRICHLET ? -1 : bc == FDW_BC_NULL_NEUMANN ? 1 : 0;
+            b.act[a][sd] = a < c->ndim ? 1 : 0;
         }
-    if (c->ndim == 3) {
-        F.act[0][0] = c->d.rank == 0;
-        F.act[0][1] = c->d.rank == c->d.world - 1;
     }
-    return F;
+    if (c->ndim == 3) {
+        b.act[0][0] = lo_z;
+        b.act[0][1] = hi_z;
+    }
+    int n = 0;
+    auto add = [&](int z0, int x0, int y0, int nz, int nx, int ny, int zero) {
+        if (nz <= 0 || nx <= 0 || ny <= 0) return;
+        b.reg[n] = {{z0, x0, y0}, {nz, nx, ny}, zero};
+        ++n;
+    };
+    const int yP = c->ndim == 3 ? P[2] : 1;
+    const int yh = c->ndim == 3 ? h : 0;
+    const int ny = c->ndim == 3 ? ext[2] : 1;
+    // ghost cells
+    if (b.act[0][0]) add(0, 0, 0, h, P[1], yP, 0);
+    if (b.act[0][1]) add(P[0] - h, 0, 0, h, P[1], yP, 0);
+    add(h, 0, 0, ext[0], h, yP, 0);
+    add(h, P[1] - h, 0, ext[0], h, yP, 0);
+    if (c->ndim == 3) {
+        add(h, h, 0, ext[0], ext[1], h, 0);
+        add(h, h, P[2] - h, ext[0], ext[1], h, 0);
+    }
+    // Dirichlet face nodes
+    if (b.act[0][0] && b.f[0][0] < 0) add(h, h, yh, 1, ext[1], ny, 1);
+    if (b.act[0][1] && b.f[0][1] < 0) add(h + ext[0] - 1, h, yh, 1, ext[1], ny, 1);
+    if (b.f[1][0] < 0) add(h, h, yh, ext[0], 1, ny, 1);
+    if (b.f[1][1] < 0) add(h, h + ext[1] - 1, yh, ext[0], 1, ny, 1);
+    if (c->ndim == 3) {
+        if (b.f[2][0] < 0) add(h, h, h, ext[0], ext[1], 1, 1);
+        if (b.f[2][1] < 0) add(h, h, h + ext[2] - 1, ext[0], ext[1], 1, 1);
+    }
+    b.n_regions = n;
+    b.start[0] = 0;
+    for (int r = 0; r < n; ++r)
+        b.start[r + 1] = b.start[r] + (long long)b.reg[r].n[0] * b.reg[r].n[1] * b.reg[r].n[2];
+    return b;
+}
+
+template <typename T>
+fdw_status launch_faces_t(fdw_solver* c, int lv) {
+    const fdw::BoundaryArgs b = boundary_args(c);
+    if (b.n_regions == 0) return FDW_OK;
+    long long mx = 0;
+    for (int r = 0; r < b.n_regions; ++r) mx = std::max(mx, b.start[r + 1] - b.start[r]);
+    dim3 grid((unsigned)((mx + 255) / 256), (unsigned)b.n_regions);
+    fdw::boundary_kernel<T><<<grid, 256, 0, c->stream>>>(static_cast<T*>(c->lvl[lv]), b, c->ctrl);
+    CHECK_LAUNCH();
+    return FDW_OK;
+}
+
+fdw_status launch_faces(fdw_solver* c, int lv) {
+    return c->tsize == 4 ? launch_faces_t<float>(c, lv) : launch_faces_t<double>(c, lv);
 }
 
 template <typename T>
@@ -181,7 +243,16 @@ SweepArgs<T> sweep_args(fdw_solver* c, int src, int dst) {
     a.nz = (int)c->nzl;
     a.nx = (int)c->nxl;
     a.ny = (int)c->nyl;
-    a.faces = faces_of(c);
+    for (int ax = 0; ax < 3; ++ax)
+        for (int sd = 0; sd < 2; ++sd) {
+            const int bc = c->d.bc[ax][sd];
+            a.gf[ax][sd] = bc == FDW_BC_NULL_DIRICHLET ? -1 : bc == FDW_BC_NULL_NEUMANN ? 1 : 0;
+            a.gact[ax][sd] = ax < c->ndim ? 1 : 0;
+        }
+    if (c->ndim == 3) {
+        a.gact[0][0] = c->d.rank == 0;
+        a.gact[0][1] = c->d.rank == c->d.world - 1;
+    }
     a.ctrl = c->ctrl;
     return a;
 }
@@ -240,6 +311,117 @@ bool launch_zmarch(fdw_solver* c, const SweepArgs<T>& a) {
 
 bool zmarch_supported(int R) { return R == 1 || R == 2 || R == 4; }
 
+constexpr int TMA_BX = 16;
+
+template <typename T, int R, bool EX, int MINB>
+const void* tma_fn() {
+    return (const void*)fdw::sweep3d_tma<T, R, TMA_BX, EX, MINB>;
+}
+
+template <typename T>
+int tma_smem(int R) {
+    switch (R) {
+        case 1: return fdw::TmaShape<T, 1, TMA_BX>::SMEM;
+        case 2: return fdw::TmaShape<T, 2, TMA_BX>::SMEM;
+        default: return fdw::TmaShape<T, 4, TMA_BX>::SMEM;
+    }
+}
+
+// minb: 2 or 3 resident CTAs requested from ptxas (register cap 128 / 80)
+template <typename T>
+const void* tma_kernel(int R, bool ex, int minb) {
+#define TK(RR)                                                                                  \
+    if (R == RR)                                                                                \
+        return ex ? (minb == 3 ? tma_fn<T, RR, true, 3>() : tma_fn<T, RR, true, 2>())            \
+                  : (minb == 3 ? tma_fn<T, RR, false, 3>() : tma_fn<T, RR, false, 2>());
+    TK(1)
+    TK(2)
+    TK(4)
+#undef TK
+    return nullptr;
+}
+
+template <typename T, bool EX>
+bool launch_tma(fdw_solver* c, const SweepArgs<T>& a, int src, int dst) {
+    using S4 = fdw::TmaShape<T, 4, TMA_BX>;
+    dim3 block(S4::NTY, TMA_BX);
+    dim3 grid((unsigned)((c->nyl + S4::TYW - 1) / S4::TYW), (unsigned)((c->nxl + TMA_BX - 1) / TMA_BX),
+              (unsigned)c->zseg);
+    const int col_base = (int)(c->base + c->R);
+    const int smem = tma_smem<T>(c->R);
+    switch (c->R) {
+#define LT(RR)                                                                                          \
+    case RR:                                                                                            \
+        if (c->tma_minb == 3)                                                                           \
+            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3><<<grid, block, smem, c->stream>>>(                   \
+                a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, col_base);                             \
+        else                                                                                            \
+            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2><<<grid, block, smem, c->stream>>>(                   \
+                a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, col_base);                             \
+        return true;
+        LT(1)
+        LT(2)
+        LT(4)
+#undef LT
+        default: return false;
+    }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3D map over one pitched level: dims (ld, rows_alloc, planes), box (bw, bh, 1)
+bool make_map(const fdw_solver* c, CUtensorMap* m, void* base, int bw, int bh) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)c->ld, (cuuint64_t)c->rows_alloc, (cuuint64_t)(c->Lz + 1)};
+    const cuuint64_t strides[2] = {(cuuint64_t)c->ld * c->tsize, (cuuint64_t)c->plane * c->tsize};
+    const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(m, c->tsize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                          base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <typename T>
+bool make_maps_t(fdw_solver* c) {
+    int uw, uh, pw, ph;
+    switch (c->R) {
+#define SH(RR)                                                                   \
+    case RR:                                                                     \
+        uw = fdw::TmaShape<T, RR, TMA_BX>::UW;                                    \
+        uh = fdw::TmaShape<T, RR, TMA_BX>::UH;                                    \
+        pw = fdw::TmaShape<T, RR, TMA_BX>::TYW;                                   \
+        ph = TMA_BX;                                                             \
+        break;
+        SH(1)
+        SH(2)
+        SH(4)
+#undef SH
+        default: return false;
+    }
+    bool ok = true;
+    for (int l = 0; l < 2; ++l) {
+        ok &= make_map(c, &c->tm_u[l], c->lvl[l], uw, uh);
+        ok &= make_map(c, &c->tm_p[l], c->lvl[l], pw, ph);
+    }
+    ok &= make_map(c, &c->tm_c, c->c2dt2, pw, ph);
+    ok &= make_map(c, &c->tm_e, c->eta, pw, ph);
+    return ok;
+}
+
 template <typename T>
 int zmarch_occupancy(int R, bool exact) {
     constexpr int BX = 16;
@@ -260,10 +442,17 @@ int zmarch_occupancy(int R, bool exact) {
 }
 
 template <typename T>
-fdw_status launch_sweep_t(fdw_solver* c, int src, int dst) {
+fdw_status launch_sweep_t(fdw_solver* c, int src, int dst, bool virt) {
     const SweepArgs<T> a = sweep_args<T>(c, src, dst);
     const bool ex = c->d.math == FDW_MATH_EXACT;
-    if (c->variant == FDW_KERNEL_ZMARCH) {
+    if (c->variant == FDW_KERNEL_TMA && !virt) {
+        // stored-ghost step (caller-uploaded level): the LDG-fed Z-march
+        const bool ok = ex ? launch_zmarch<T, true>(c, a) : launch_zmarch<T, false>(c, a);
+        if (!ok) return fail(c, FDW_EINVAL, "zmarch kernel not built for radius %d", c->R);
+    } else if (c->variant == FDW_KERNEL_TMA) {
+        const bool ok = ex ? launch_tma<T, true>(c, a, src, dst) : launch_tma<T, false>(c, a, src, dst);
+        if (!ok) return fail(c, FDW_EINVAL, "TMA kernel not built for radius %d", c->R);
+    } else if (c->variant == FDW_KERNEL_ZMARCH) {
         const bool ok = ex ? launch_zmarch<T, true>(c, a) : launch_zmarch<T, false>(c, a);
         if (!ok) return fail(c, FDW_EINVAL, "zmarch kernel not built for radius %d", c->R);
     } else {
@@ -276,8 +465,8 @@ fdw_status launch_sweep_t(fdw_solver* c, int src, int dst) {
     return FDW_OK;
 }
 
-fdw_status launch_sweep(fdw_solver* c, int src, int dst) {
-    return c->tsize == 4 ? launch_sweep_t<float>(c, src, dst) : launch_sweep_t<double>(c, src, dst);
+fdw_status launch_sweep(fdw_solver* c, int src, int dst, bool virt) {
+    return c->tsize == 4 ? launch_sweep_t<float>(c, src, dst, virt) : launch_sweep_t<double>(c, src, dst, virt);
 }
 
 template <typename T>
@@ -286,8 +475,7 @@ fdw_status launch_inject_t(fdw_solver* c, int dst, int k) {
     const int tb = 128;
     fdw::inject_kernel<T, true><<<(c->n_tgt + tb - 1) / tb, tb, 0, c->stream>>>(
         static_cast<T*>(c->lvl[dst]), static_cast<const T*>(c->c2dt2), static_cast<const T*>(c->eta),
-        c->d.dt, c->d_tgt, c->d_ent_off, c->d_ent_w, c->d_wavelet, c->n_wavelet, c->n_tgt, k, c->ctrl,
-        faces_of(c), c->origin, c->R);
+        c->d.dt, c->d_tgt, c->d_ent_off, c->d_ent_w, c->d_wavelet, c->n_wavelet, c->n_tgt, k, c->ctrl);
     CHECK_LAUNCH();
     return FDW_OK;
 }
@@ -300,7 +488,8 @@ fdw_status launch_inject(fdw_solver* c, int dst, int k) {
 // For Z-slabs the Z phase runs only on global faces and the X/Y phases skip
 // the internal ghost planes (those arrive complete from the neighbour).
 template <typename T>
-fdw_status launch_boundary_t(fdw_solver* c, int lv, const Ctrl* ctrl) {
+fdw_status launch_boundary_t(fdw_solver* c, int lv, int mode) {
+    const Ctrl* ctrl = c->ctrl;
     T* f = static_cast<T*>(c->lvl[lv]);
     const int h = c->R;
     const int tb = 256;
@@ -309,7 +498,7 @@ fdw_status launch_boundary_t(fdw_solver* c, int lv, const Ctrl* ctrl) {
         const long long n = (long long)n1 * n2;
         if (n <= 0 || (!do_lo && !do_hi)) return FDW_OK;
         fdw::ghost_lines<T><<<(unsigned)((n + tb - 1) / tb), tb, 0, c->stream>>>(
-            f, origin_pad, sa, n_ext, h, s1, n1, s2, n2, bc_lo, bc_hi, do_lo, do_hi, ctrl);
+            f, origin_pad, sa, n_ext, h, s1, n1, s2, n2, bc_lo, bc_hi, do_lo, do_hi, ctrl, mode);
         CHECK_LAUNCH();
         return FDW_OK;
     };
@@ -343,8 +532,8 @@ fdw_status launch_boundary_t(fdw_solver* c, int lv, const Ctrl* ctrl) {
     return FDW_OK;
 }
 
-fdw_status launch_boundary(fdw_solver* c, int lv, const Ctrl* ctrl) {
-    return c->tsize == 4 ? launch_boundary_t<float>(c, lv, ctrl) : launch_boundary_t<double>(c, lv, ctrl);
+fdw_status launch_boundary(fdw_solver* c, int lv, int mode) {
+    return c->tsize == 4 ? launch_boundary_t<float>(c, lv, mode) : launch_boundary_t<double>(c, lv, mode);
 }
 
 ncclDataType_t nccl_type(const fdw_solver* c) { return c->tsize == 4 ? ncclFloat : ncclDouble; }
@@ -388,39 +577,69 @@ fdw_status launch_receivers(fdw_solver* c, int lv, int row_add) {
 
 // Health reduction over this rank's owned padded planes (global faces keep
 // their ghost planes; internal ghost planes belong to the neighbour).
+// check_health / max_abs (kernel.hpp:265-273, :456-458): a scan of the
+// extended points gives max |u| (ghost cells only repeat those magnitudes or
+// hold 0); only if a non-finite value exists are the ghost cells materialised
+// (exact apply_boundary) and the padded slab rescanned for the first
+// non-finite flat index, as the reference's padded scan returns it.
 template <typename T>
 fdw_status launch_health_t(fdw_solver* c, int lv, int honor_abort) {
+    // a caller-uploaded level keeps its own ghost values: scan it as stored
+    const bool raw = c->gstate[lv] == 2;
     fdw::health_reset<<<1, 1, 0, c->stream>>>(c->ctrl, honor_abort);
     CHECK_LAUNCH();
     const T* u = static_cast<const T*>(c->lvl[lv]);
+    const int h = c->R;
     long long p_lo = 0, p_hi = 1, n_rows, n_cols;
-    unsigned long long gp0 = 0, gp_lo = 0, gp_hi = 0;
+    unsigned long long gp_lo = 0, gp_hi = 0;
+    int ext_planes = 1, ext_rows, ext_cols, e_p0 = 0;
     if (c->ndim == 3) {
-        p_lo = c->d.rank > 0 ? c->R : 0;
-        p_hi = c->d.rank < c->d.world - 1 ? c->Lz - c->R : c->Lz;
-        gp0 = c->d.z_begin + p_lo;  // global padded plane of local plane p_lo
-        gp_lo = c->d.z_begin;       // global padded plane of local plane 0
+        p_lo = c->d.rank > 0 ? h : 0;
+        p_hi = c->d.rank < c->d.world - 1 ? c->Lz - h : c->Lz;
+        gp_lo = c->d.z_begin;  // global padded plane of local plane 0
         gp_hi = c->d.z_begin + c->Lz;
         n_rows = c->P[1];
         n_cols = c->P[2];
+        ext_planes = (int)c->nzl;
+        e_p0 = h;
+        ext_rows = (int)c->nxl;
+        ext_cols = (int)c->nyl;
     } else {
         n_rows = c->P[0];
         n_cols = c->P[1];
+        ext_rows = (int)c->nzl;
+        ext_cols = (int)c->nxl;
     }
-    const long long total_rows = (p_hi - p_lo) * n_rows;
-    const int blocks = (int)std::min<long long>(total_rows, (long long)c->sm_count * 8);
-    fdw::health_kernel<T><<<blocks, 256, 0, c->stream>>>(
-        u, c->origin_pad + p_lo * c->plane, c->ld, c->plane, (int)(p_hi - p_lo), (int)n_rows,
-        (int)n_cols, gp0, (unsigned long long)c->P[1], (unsigned long long)c->P[2], c->ndim == 3,
-        c->ctrl, honor_abort);
-    CHECK_LAUNCH();
+    const unsigned long long P1 = (unsigned long long)c->P[1], P2 = (unsigned long long)c->P[2];
+    const int is3d = c->ndim == 3;
+    if (!raw) {
+        const long long rows = (long long)ext_planes * ext_rows;
+        const int blocks = (int)std::min<long long>(rows, (long long)c->sm_count * 8);
+        fdw::health_kernel<T><<<blocks, 256, 0, c->stream>>>(u, c->origin_pad, c->ld, c->plane, e_p0, ext_planes, h,
+                                                             ext_rows, h, ext_cols, gp_lo, P1, P2, is3d, c->ctrl,
+                                                             honor_abort, 0);
+        CHECK_LAUNCH();
+    }
     if (c->d.world > 1) {
         NC(ncclAllReduce(&c->ctrl->bad_idx, &c->ctrl->bad_idx, 1, ncclUint64, ncclMin, c->comm, c->stream));
         NC(ncclAllReduce(&c->ctrl->max_bits, &c->ctrl->max_bits, 1, ncclUint64, ncclMax, c->comm, c->stream));
     }
-    fdw::health_classify<T><<<1, 1, 0, c->stream>>>(
-        u, c->ctrl, c->origin_pad, c->ld, c->plane, gp_lo, gp_hi, (unsigned long long)c->P[1],
-        (unsigned long long)c->P[2], c->ndim == 3, honor_abort);
+    {
+        if (!raw) {
+            fdw_status s = launch_boundary(c, lv, 2);
+            if (s) return s;
+        }
+        const long long rows = (p_hi - p_lo) * n_rows;
+        const int blocks = (int)std::min<long long>(rows, (long long)c->sm_count * 8);
+        fdw::health_kernel<T><<<blocks, 256, 0, c->stream>>>(u, c->origin_pad, c->ld, c->plane, (int)p_lo,
+                                                             (int)(p_hi - p_lo), 0, (int)n_rows, 0, (int)n_cols,
+                                                             gp_lo, P1, P2, is3d, c->ctrl, honor_abort, raw ? 0 : 1);
+        CHECK_LAUNCH();
+    }
+    if (c->d.world > 1)
+        NC(ncclAllReduce(&c->ctrl->bad_idx, &c->ctrl->bad_idx, 1, ncclUint64, ncclMin, c->comm, c->stream));
+    fdw::health_classify<T><<<1, 1, 0, c->stream>>>(u, c->ctrl, c->origin_pad, c->ld, c->plane, gp_lo, gp_hi, P1, P2,
+                                                    is3d, honor_abort);
     CHECK_LAUNCH();
     if (c->d.world > 1)
         NC(ncclAllReduce(&c->ctrl->kind, &c->ctrl->kind, 1, ncclUint32, ncclMax, c->comm, c->stream));
@@ -453,22 +672,29 @@ struct Mark {
 
 // One Solver::step (kernel.hpp:226-233) with relative index k inside a chunk;
 // `src` is the current level before the step.
-fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record) {
+// Virtual-ghost path for a step reading level `src`: only the TMA kernel, and
+// only when src's stored ghosts are not caller-provided raw values.
+bool virtual_step(const fdw_solver* c, int gstate_src) {
+    return c->variant == FDW_KERNEL_TMA && gstate_src != 2;
+}
+
+fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
     const int dst = 1 - src;
     fdw_status s;
-    { Mark m(c, 0); if ((s = launch_sweep(c, src, dst))) return s; }
+    { Mark m(c, 0); if ((s = launch_sweep(c, src, dst, virt))) return s; }
     { Mark m(c, 1); if ((s = launch_inject(c, dst, k))) return s; }
-    // swap: dst is now the current level; its ghost cells were written by the
-    // sweep and injection kernels (apply_boundary fused, see fdw::Faces)
+    // swap: dst is now the current level
+    if (!virt) { Mark m(c, 2); if ((s = launch_faces(c, dst))) return s; }
     if (c->d.world > 1) { Mark m(c, 5); if ((s = launch_halo(c, dst))) return s; }
     if (record) { Mark m(c, 3); if ((s = launch_receivers(c, dst, k + 1))) return s; }
     return FDW_OK;
 }
 
-fdw_status enqueue_chunk(fdw_solver* c, unsigned long long L, int cur0, bool check, bool record) {
+fdw_status enqueue_chunk(fdw_solver* c, unsigned long long L, int cur0, bool check, bool record, bool first_virt,
+                         bool rest_virt) {
     fdw_status s;
     for (unsigned long long k = 0; k < L; ++k)
-        if ((s = enqueue_step(c, (int)k, cur0 ^ (int)(k & 1), record))) return s;
+        if ((s = enqueue_step(c, (int)k, cur0 ^ (int)(k & 1), record, k == 0 ? first_virt : rest_virt))) return s;
     fdw::step_advance<<<1, 1, 0, c->stream>>>(c->ctrl, L);
     CHECK_LAUNCH();
     if (check) {
@@ -483,18 +709,20 @@ fdw_status enqueue_chunk(fdw_solver* c, unsigned long long L, int cur0, bool che
 
 fdw_status run_chunk(fdw_solver* c, unsigned long long L, bool check, bool record) {
     const int cur0 = c->cur;
+    const bool first_virt = virtual_step(c, c->gstate[cur0]);
+    const bool rest_virt = virtual_step(c, 0);
     if (L < 8 || c->prof) {
-        fdw_status s = enqueue_chunk(c, L, cur0, check, record);
+        fdw_status s = enqueue_chunk(c, L, cur0, check, record, first_virt, rest_virt);
         if (s) return s;
     } else {
-        const auto key = std::make_tuple(L, cur0, (int)check, (int)record);
+        const auto key = std::make_tuple(L, cur0 | (first_virt ? 2 : 0), (int)check, (int)record);
         auto it = c->graphs.find(key);
         if (it == c->graphs.end()) {
             cudaGraph_t g;
             CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
             c->capturing = true;
             c->capture_kernels = 0;
-            fdw_status s = enqueue_chunk(c, L, cur0, check, record);
+            fdw_status s = enqueue_chunk(c, L, cur0, check, record, first_virt, rest_virt);
             c->capturing = false;
             cudaError_t e = cudaStreamEndCapture(c->stream, &g);
             if (s) return s;
@@ -508,8 +736,23 @@ fdw_status run_chunk(fdw_solver* c, unsigned long long L, bool check, bool recor
         CU(cudaGraphLaunch(it->second, c->stream));
         c->launches += c->graph_kernels[key];
     }
+    // ghost state of the levels written by this chunk
+    for (unsigned long long k = 0; k < L && k < 2; ++k) {
+        const unsigned long long kk = L - 1 - k;  // last two steps
+        const int dst = 1 - (cur0 ^ (int)(kk & 1));
+        c->gstate[dst] = (kk == 0 ? first_virt : rest_virt) ? 1 : 0;
+    }
     c->cur = cur0 ^ (int)(L & 1);
     c->host_step += L;
+    return FDW_OK;
+}
+
+// Materialises the stored ghost cells of a level whose ghosts are virtual.
+fdw_status settle_ghosts(fdw_solver* c, int lv) {
+    if (c->gstate[lv] != 1) return FDW_OK;
+    fdw_status s = launch_boundary(c, lv, 0);
+    if (s) return s;
+    c->gstate[lv] = 0;
     return FDW_OK;
 }
 
@@ -534,7 +777,8 @@ int pick_zseg(fdw_solver* c, int occ) {
         const double waves = std::ceil(ctas / resident);
         const double fill = ctas / (waves * resident);
         const double warm = 1.0 - 0.2 * (2.0 * c->R * s) / (double)c->nzl;
-        const double score = fill * warm;
+        const double balance = std::min(1.0, waves / 6.0);  // many short waves even out SM load
+        const double score = fill * warm * (0.9 + 0.1 * balance);
         if (score > best + 1e-9) {
             best = score;
             best_s = s;
@@ -812,12 +1056,40 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
     // kernel selection
     int variant = d.variant;
     if (variant == FDW_KERNEL_AUTO)
-        variant = (c->ndim == 3 && zmarch_supported(R)) ? FDW_KERNEL_ZMARCH : FDW_KERNEL_SIMPLE;
-    if (variant == FDW_KERNEL_ZMARCH && (c->ndim != 3 || !zmarch_supported(R))) variant = FDW_KERNEL_SIMPLE;
+        variant = (c->ndim == 3 && zmarch_supported(R)) ? FDW_KERNEL_TMA : FDW_KERNEL_SIMPLE;
+    if ((variant == FDW_KERNEL_ZMARCH || variant == FDW_KERNEL_TMA) && (c->ndim != 3 || !zmarch_supported(R)))
+        variant = FDW_KERNEL_SIMPLE;
+    if (variant == FDW_KERNEL_TMA) {
+        const bool ok = c->tsize == 4 ? make_maps_t<float>(c) : make_maps_t<double>(c);
+        if (!ok) {
+            fail(c, FDW_ECUDA, "cuTensorMapEncodeTiled failed (TMA descriptors)");
+            return bail(FDW_ECUDA);
+        }
+    }
     c->variant = variant;
-    if (variant == FDW_KERNEL_ZMARCH) {
+    if (variant == FDW_KERNEL_ZMARCH || variant == FDW_KERNEL_TMA) {
         const bool ex = d.math == FDW_MATH_EXACT;
-        const int occ = c->tsize == 4 ? zmarch_occupancy<float>(R, ex) : zmarch_occupancy<double>(R, ex);
+        int occ = 1;
+        if (variant == FDW_KERNEL_ZMARCH) {
+            occ = c->tsize == 4 ? zmarch_occupancy<float>(R, ex) : zmarch_occupancy<double>(R, ex);
+        } else {
+            // prefer 3 CTAs/SM (80-register cap) unless that build spills
+            const char* env = std::getenv("FDW_TMA_MINB");
+            int minb = env ? std::atoi(env) : 0;
+            if (minb != 2 && minb != 3) {
+                cudaFuncAttributes fa{};
+                const void* f3 = c->tsize == 4 ? tma_kernel<float>(R, ex, 3) : tma_kernel<double>(R, ex, 3);
+                minb = (cudaFuncGetAttributes(&fa, f3) == cudaSuccess && fa.localSizeBytes == 0) ? 3 : 2;
+            }
+            c->tma_minb = minb;
+            const void* f = c->tsize == 4 ? tma_kernel<float>(R, ex, minb) : tma_kernel<double>(R, ex, minb);
+            const int smem = c->tsize == 4 ? tma_smem<float>(R) : tma_smem<double>(R);
+            if (!ck(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr"))
+                return bail(FDW_ECUDA);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 16 * TMA_BX, smem) != cudaSuccess || occ < 1)
+                occ = 1;
+        }
+        c->occupancy = occ;
         c->zseg = d.z_segments > 0 ? d.z_segments : pick_zseg(c, occ);
         if (c->zseg > c->nzl) c->zseg = (int)c->nzl;
     }
@@ -966,6 +1238,8 @@ fdw_status fdw_set_levels(fdw_solver* c, const void* prev, const void* curr) {
     if (s) return s;
     if (prev && (s = copy_host_to_level(c, c->lvl[1 - c->cur], prev, 0))) return s;
     if (curr && (s = copy_host_to_level(c, c->lvl[c->cur], curr, 0))) return s;
+    if (prev) c->gstate[1 - c->cur] = 2;
+    if (curr) c->gstate[c->cur] = 2;
     CU(cudaStreamSynchronize(c->stream));
     return FDW_OK;
 }
@@ -976,12 +1250,15 @@ fdw_status fdw_zero_levels(fdw_solver* c) {
     const size_t bytes = c->level_elems * c->tsize;
     CU(cudaMemsetAsync(c->lvl[0], 0, bytes, c->stream));
     CU(cudaMemsetAsync(c->lvl[1], 0, bytes, c->stream));
+    c->gstate[0] = c->gstate[1] = 0;  // all-zero levels satisfy every boundary condition
     return FDW_OK;
 }
 
 fdw_status fdw_get_levels(fdw_solver* c, void* prev, void* curr) {
     fdw_status s = prologue(c);
     if (s) return s;
+    if (prev && (s = settle_ghosts(c, 1 - c->cur))) return s;
+    if (curr && (s = settle_ghosts(c, c->cur))) return s;
     if (prev && (s = copy_level_to_host(c, prev, c->lvl[1 - c->cur]))) return s;
     if (curr && (s = copy_level_to_host(c, curr, c->lvl[c->cur]))) return s;
     CU(cudaStreamSynchronize(c->stream));
@@ -1011,8 +1288,9 @@ fdw_status fdw_get_extended(fdw_solver* c, void* out) {
 fdw_status fdw_refresh_boundary(fdw_solver* c) {
     fdw_status s = prologue(c);
     if (s) return s;
-    if ((s = launch_boundary(c, c->cur, nullptr))) return s;
+    if ((s = launch_boundary(c, c->cur, 0))) return s;
     if ((s = launch_halo(c, c->cur))) return s;
+    c->gstate[c->cur] = 0;
     CU(cudaStreamSynchronize(c->stream));
     return FDW_OK;
 }
@@ -1048,8 +1326,15 @@ fdw_status fdw_advance(fdw_solver* c, uint64_t n, uint32_t flags, uint64_t* bad_
     if ((s = read_ctrl(c))) return s;
     if (c->h_ctrl->abort) {
         // state is frozen at the failing step; restore host bookkeeping
+        const unsigned long long done = c->h_ctrl->step - start;
         c->host_step = c->h_ctrl->step;
-        c->cur = cur_start ^ (int)((c->h_ctrl->step - start) & 1);
+        c->cur = cur_start ^ (int)(done & 1);
+        // levels written by executed steps: treat their ghosts as virtual
+        // (settled from the extended values on download)
+        if (c->variant == FDW_KERNEL_TMA) {
+            c->gstate[c->cur] = 1;
+            if (done >= 2) c->gstate[1 - c->cur] = 1;
+        }
         if (bad_step) *bad_step = c->h_ctrl->bad_step;
         if (bad_max)
             *bad_max = c->h_ctrl->kind == 2 ? std::numeric_limits<double>::quiet_NaN()
@@ -1177,7 +1462,7 @@ fdw_status fdw_layout(const fdw_solver* c, uint64_t* ld, uint64_t* plane, uint64
     if (plane) *plane = (uint64_t)c->plane;
     if (base) *base = (uint64_t)c->base;
     if (planes) *planes = (uint64_t)c->Lz;
-    if (variant) *variant = c->variant | (c->zseg << 8);
+    if (variant) *variant = c->variant | (c->zseg << 8) | (c->occupancy << 16);
     return FDW_OK;
 }
 

@@ -9,8 +9,11 @@
 // proj/CMakeLists.txt:7-19).  With EXACT = false the compiler may contract.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <type_traits>
 
 namespace fdw {
 
@@ -75,72 +78,6 @@ __device__ __forceinline__ T time_update(T rhs, T uc, T c2, T prev, T eta, doubl
     return A::mul(A::sub(t, A::mul(om, prev)), iop);
 }
 
-// Per-face boundary handling fused into the producers of a level.  After the
-// sweep (and after injection for the injected points) every ghost cell of the
-// new level holds what apply_boundary (kernel.hpp:67-102) would put there:
-// the thread that owns extended point c writes each ghost cell whose mirror
-// source is c (Dirichlet -u, Neumann +u, none 0; corners take the product of
-// the per-axis factors), and Dirichlet face points are forced to +0.  Internal
-// Z faces of a slab are inactive (their ghost planes come from the neighbour).
-struct Faces {
-    int nd;                  // 2 or 3
-    int n[3];                // extended extents (local Z for slabs)
-    long long s[3];          // element strides per axis
-    signed char f[3][2];     // ghost factor per side: -1 Dirichlet, +1 Neumann, 0 none
-    unsigned char act[3][2]; // side is a physical face handled here
-};
-
-__device__ __forceinline__ bool on_dirichlet_face(const Faces& F, const int* c) {
-    bool z = false;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        if (a < F.nd) {
-            z |= F.act[a][0] && F.f[a][0] < 0 && c[a] == 0;
-            z |= F.act[a][1] && F.f[a][1] < 0 && c[a] == F.n[a] - 1;
-        }
-    }
-    return z;
-}
-
-__device__ __forceinline__ bool near_face(const Faces& F, const int* c, int R) {
-    bool near = false;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-        if (a < F.nd) near |= (c[a] <= R) || (c[a] >= F.n[a] - 1 - R);
-    return near;
-}
-
-template <typename T>
-__device__ void ghost_writes(T* out, long long i, const int* c, T v, const Faces& F, int R) {
-    long long d[3];
-    int f[3];
-    int m = 0;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        if (a >= F.nd) continue;
-        const int ca = c[a], na = F.n[a];
-        if (F.act[a][0] && ca >= 1 && ca <= R) {
-            d[m] = -2LL * ca * F.s[a];
-            f[m] = F.f[a][0];
-            ++m;
-        } else if (F.act[a][1] && ca >= na - 1 - R && ca <= na - 2) {
-            d[m] = 2LL * (na - 1 - ca) * F.s[a];
-            f[m] = F.f[a][1];
-            ++m;
-        }
-    }
-    for (int mask = 1; mask < (1 << m); ++mask) {
-        long long dd = 0;
-        int ff = 1;
-        for (int b = 0; b < m; ++b)
-            if (mask & (1 << b)) {
-                dd += d[b];
-                ff *= f[b];
-            }
-        out[i + dd] = ff == 0 ? T(0) : (ff < 0 ? -v : v);
-    }
-}
-
 template <typename T>
 struct SweepArgs {
     const T* __restrict__ u;      // current level
@@ -152,7 +89,10 @@ struct SweepArgs {
     double dt;
     long long ld, plane, origin;  // element strides; offset of extended (0,0,0)
     int nz, nx, ny;               // extended extents (local Z for slabs; 2D: rows nz, cols nx)
-    Faces faces;
+    // virtual ghosts (FDW_KERNEL_TMA): mirror factor per face (-1 Dirichlet,
+    // +1 Neumann, 0 none) and whether the face is physical on this rank
+    int gf[3][2];
+    int gact[3][2];
     const Ctrl* ctrl;
 };
 
@@ -177,13 +117,7 @@ __global__ void __launch_bounds__(256) sweep3d_simple(SweepArgs<T> a) {
         ly = A::add(ly, A::mul(a.v[j], A::add(__ldg(u + i + j), __ldg(u + i - j))));
     }
     const T rhs = A::add(A::add(A::mul(lz, a.ih[0]), A::mul(lx, a.ih[1])), A::mul(ly, a.ih[2]));
-    T res = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
-    const int c[3] = {iz, ix, iy};
-    if (near_face(a.faces, c, R)) {
-        if (on_dirichlet_face(a.faces, c)) res = T(0);
-        ghost_writes(a.out, i, c, res, a.faces, R);
-    }
-    a.out[i] = res;
+    a.out[i] = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
 }
 
 // sweep_2d<false>, kernel.hpp:344-379 -- rows are Z, the fast axis is X.
@@ -204,13 +138,7 @@ __global__ void __launch_bounds__(256) sweep2d_simple(SweepArgs<T> a) {
         lx = A::add(lx, A::mul(a.v[j], A::add(__ldg(u + i + j), __ldg(u + i - j))));
     }
     const T rhs = A::add(A::mul(lz, a.ih[0]), A::mul(lx, a.ih[1]));
-    T res = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
-    const int c[3] = {iz, ix, 0};
-    if (near_face(a.faces, c, R)) {
-        if (on_dirichlet_face(a.faces, c)) res = T(0);
-        ghost_writes(a.out, i, c, res, a.faces, R);
-    }
-    a.out[i] = res;
+    a.out[i] = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
 }
 
 // ---------------------------------------------------------------------------
@@ -364,18 +292,6 @@ __global__ void __launch_bounds__(ZMarchShape<T, BX>::THREADS)
         }
         if (xin) {
             T* o = a.out + col0 + (long long)z * plane;
-            const int c0[3] = {z, x, y0};
-            const int c1[3] = {z, x, y0 + V - 1};
-            if (near_face(a.faces, c0, R) || near_face(a.faces, c1, R)) {
-#pragma unroll
-                for (int e = 0; e < V; ++e) {
-                    const int c[3] = {z, x, y0 + e};
-                    if (y0 + e < a.ny) {
-                        if (on_dirichlet_face(a.faces, c)) res.e[e] = T(0);
-                        ghost_writes(a.out, col0 + (long long)z * plane + e, c, res.e[e], a.faces, R);
-                    }
-                }
-            }
             if (y0 + V <= a.ny) {
                 st16(o, res);
             } else {
@@ -389,6 +305,348 @@ __global__ void __launch_bounds__(ZMarchShape<T, BX>::THREADS)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// TMA + mbarrier helpers (inline PTX, sm_90+/sm_100a)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "FDW_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra FDW_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <typename T, int R, int BX>
+struct TmaShape {
+    static constexpr int V = 16 / sizeof(T);
+    static constexpr int NTY = 16;
+    static constexpr int TYW = NTY * V;                  // tile width (elements)
+    static constexpr int HY = ((R + V - 1) / V) * V;     // Y halo, whole vectors
+    static constexpr int UW = TYW + 2 * HY;              // U tile row (elements)
+    static constexpr int UH = BX + 2 * R;                // U tile rows
+    static constexpr int NU = R + 2;                     // U ring: planes z .. z+R, +1 in flight
+    static constexpr int NP = 2;                         // prev/c2dt2/eta ring
+    static constexpr int U_BOX = UW * UH * (int)sizeof(T);
+    static constexpr int P_BOX = TYW * BX * (int)sizeof(T);
+    static constexpr int U_STRIDE = (U_BOX + 127) / 128 * 128;
+    static constexpr int P_STRIDE = (P_BOX + 127) / 128 * 128;
+    static constexpr int BAR_OFF = NU * U_STRIDE + NP * 3 * P_STRIDE;
+    static constexpr int SMEM = BAR_OFF + (NU + NP) * 8;
+    static constexpr int THREADS = NTY * BX;
+};
+
+// sweep_3d<false>, kernel.hpp:381-424 -- TMA-fed 2.5D Z-march.  Per CTA a
+// BX x TYW (X, Y) column, one Z segment.  One elected thread streams, per
+// plane, the u tile with its radius-R X/Y halos and the prev/c2dt2/eta tiles
+// into shared-memory rings with cp.async.bulk.tensor (completion on
+// mbarriers); the 2R+1 Z neighbours of each thread's V outputs live in a
+// register queue fed from the ring (head = plane z+R).  No per-thread global
+// loads on the hot path; one __syncthreads per plane recycles ring stages.
+template <typename T, int R, int BX, bool EXACT, int MINB>
+__global__ void __launch_bounds__(TmaShape<T, R, BX>::THREADS, MINB)
+    sweep3d_tma(SweepArgs<T> a, const __grid_constant__ CUtensorMap tu, const __grid_constant__ CUtensorMap tp,
+                const __grid_constant__ CUtensorMap tc, const __grid_constant__ CUtensorMap te, int col_base) {
+    using A = Ar<T, EXACT>;
+    using S = TmaShape<T, R, BX>;
+    constexpr int V = S::V, NTY = S::NTY, TYW = S::TYW, HY = S::HY, HYV = HY / V, UW = S::UW, NU = S::NU;
+    constexpr int THREADS = S::THREADS;
+    using VT = Vec<T, V>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long* barU = reinterpret_cast<unsigned long long*>(smem + S::BAR_OFF);
+    unsigned long long* barP = barU + NU;
+
+    if (a.ctrl->abort) return;
+    const int ty = threadIdx.x, tx = threadIdx.y, tid = tx * NTY + ty;
+    const int ty0 = blockIdx.x * TYW;
+    const int tx0 = blockIdx.y * BX;
+    const int y0 = ty0 + ty * V;
+    const int x = tx0 + tx;
+    const int nz = a.nz, nx = a.nx, ny = a.ny;
+    const int zs = (int)((long long)nz * blockIdx.z / gridDim.z);
+    const int ze = (int)((long long)nz * (blockIdx.z + 1) / gridDim.z);
+    const long long plane = a.plane;
+    const long long col0 = a.origin + (long long)x * a.ld + y0;
+
+    // Virtual Z ghosts on physical Z faces: plane p outside [0, nz) reads its
+    // mirror plane scaled by the face factor (apply_boundary, kernel.hpp:84-97).
+    const bool zlo = a.gact[0][0], zhi = a.gact[0][1];
+    auto zsrc = [&](int p) {
+        if (p < 0 && zlo) return -p;
+        if (p >= nz && zhi) return 2 * (nz - 1) - p;
+        return p;
+    };
+    auto mir = [](int f, T v) { return f == 0 ? T(0) : (f < 0 ? -v : v); };
+
+    auto u_stage = [&](int k) { return reinterpret_cast<T*>(smem + (k % NU) * S::U_STRIDE); };
+    auto p_stage = [&](int k, int which) {
+        return reinterpret_cast<T*>(smem + NU * S::U_STRIDE + ((k & 1) * 3 + which) * S::P_STRIDE);
+    };
+    auto issue_u = [&](int k) {  // tile of plane zs + k (mirrored plane beyond a physical Z face)
+        unsigned long long* b = &barU[k % NU];
+        mbar_expect_tx(b, S::U_BOX);
+        tma_load_3d(u_stage(k), &tu, col_base + ty0 - HY, tx0, zsrc(zs + k) + R, b);
+    };
+    auto issue_p = [&](int k) {
+        unsigned long long* b = &barP[k & 1];
+        mbar_expect_tx(b, 3 * S::P_BOX);
+        const int c0 = col_base + ty0, c1 = tx0 + R, c2 = zs + k + R;
+        tma_load_3d(p_stage(k, 0), &tp, c0, c1, c2, b);
+        tma_load_3d(p_stage(k, 1), &tc, c0, c1, c2, b);
+        tma_load_3d(p_stage(k, 2), &te, c0, c1, c2, b);
+    };
+
+    if (tid == 0) {
+        for (int k = 0; k < NU; ++k) mbar_init(&barU[k], 1);
+        for (int k = 0; k < S::NP; ++k) mbar_init(&barP[k], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int k = 0; k <= R; ++k) issue_u(k);  // planes zs .. zs+R
+        issue_p(0);
+    }
+    VT q[2 * R + 1];
+#pragma unroll
+    for (int k = 0; k < 2 * R; ++k) {
+        const int p = zs - R + k;
+        q[k] = ldg16(a.u + col0 + (long long)zsrc(p) * plane);
+        if ((p < 0 && zlo) || (p >= nz && zhi)) {
+            const int f = p < 0 ? a.gf[0][0] : a.gf[0][1];
+#pragma unroll
+            for (int e = 0; e < V; ++e) q[k].e[e] = mir(f, q[k].e[e]);
+        }
+    }
+
+    // Virtual X/Y ghosts: CTAs whose halo crosses a physical X/Y face patch
+    // the halo rows/columns of the staged tile from their mirror images
+    // (one extra __syncthreads per plane, edge CTAs only).
+    const bool pxl = a.gact[1][0] && tx0 == 0;
+    const bool pxh = a.gact[1][1] && tx0 + BX + R > nx;
+    const bool pyl = a.gact[2][0] && ty0 == 0;
+    const bool pyh = a.gact[2][1] && ty0 + TYW + HY > ny;
+    const bool edge_tile = pxl || pxh || pyl || pyh;
+    auto patch = [&](T* U) {
+        if (pxl) {  // rows x = -k <- row k
+            const int f = a.gf[1][0];
+            for (int i = tid; i < R * TYW; i += THREADS) {
+                const int k = i / TYW + 1, c = HY + i % TYW;
+                U[(R - k) * UW + c] = mir(f, U[(R + k) * UW + c]);
+            }
+        }
+        if (pxh) {  // rows x in [nx, nx+R) inside the tile
+            const int f = a.gf[1][1];
+            for (int i = tid; i < R * TYW; i += THREADS) {
+                const int xg = nx + i / TYW, c = HY + i % TYW;
+                const int r = xg - tx0 + R;
+                if (r < BX + 2 * R) U[r * UW + c] = mir(f, U[(2 * (nx - 1) - xg - tx0 + R) * UW + c]);
+            }
+        }
+        if (pyl) {  // columns y = -k <- column k
+            const int f = a.gf[2][0];
+            for (int i = tid; i < R * BX; i += THREADS) {
+                const int k = i % R + 1, r = R + i / R;
+                U[r * UW + HY - k] = mir(f, U[r * UW + HY + k]);
+            }
+        }
+        if (pyh) {  // columns y in [ny, ny+R) inside the tile
+            const int f = a.gf[2][1];
+            for (int i = tid; i < R * BX; i += THREADS) {
+                const int yg = ny + i % R, r = R + i / R;
+                const int c = yg - ty0 + HY;
+                if (c < UW) U[r * UW + c] = mir(f, U[r * UW + (2 * (ny - 1) - yg - ty0 + HY)]);
+            }
+        }
+    };
+
+    const bool xin = x < nx;
+    const int nit = ze - zs;
+    for (int it = 0; it < nit; ++it) {
+        const int z = zs + it;
+        if (it > 0) __syncthreads();  // stages of plane z-1 are free
+        if (tid == 0 && it + 1 < nit) {
+            issue_u(it + 1 + R);
+            issue_p(it + 1);
+        }
+        const int kh = it + R;
+        mbar_wait(&barU[kh % NU], (kh / NU) & 1);
+        q[2 * R] = *reinterpret_cast<const VT*>(u_stage(kh) + (R + tx) * UW + HY + ty * V);
+        if (zhi && z + R >= nz) {  // head is a mirrored plane (uniform branch)
+#pragma unroll
+            for (int e = 0; e < V; ++e) q[2 * R].e[e] = mir(a.gf[0][1], q[2 * R].e[e]);
+        }
+        mbar_wait(&barU[it % NU], (it / NU) & 1);
+        mbar_wait(&barP[it & 1], (it >> 1) & 1);
+        T* U0 = u_stage(it);
+        if (edge_tile) {
+            patch(U0);
+            __syncthreads();
+        }
+
+        T lz[V], lx[V], ly[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            lz[e] = A::mul(a.v[0], q[R].e[e]);
+            lx[e] = lz[e];
+            ly[e] = lz[e];
+        }
+        T w[2 * HY + V];
+#pragma unroll
+        for (int k = 0; k < 2 * HYV + 1; ++k) {
+            const VT t = *reinterpret_cast<const VT*>(U0 + (R + tx) * UW + ty * V + k * V);
+#pragma unroll
+            for (int e = 0; e < V; ++e) w[k * V + e] = t.e[e];
+        }
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+            const VT xp = *reinterpret_cast<const VT*>(U0 + (R + tx + j) * UW + HY + ty * V);
+            const VT xm = *reinterpret_cast<const VT*>(U0 + (R + tx - j) * UW + HY + ty * V);
+            const T vj = a.v[j];
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                lz[e] = A::add(lz[e], A::mul(vj, A::add(q[R + j].e[e], q[R - j].e[e])));
+                lx[e] = A::add(lx[e], A::mul(vj, A::add(xp.e[e], xm.e[e])));
+                ly[e] = A::add(ly[e], A::mul(vj, A::add(w[HY + e + j], w[HY + e - j])));
+            }
+        }
+        const int po = tx * TYW + ty * V;
+        const VT pc = *reinterpret_cast<const VT*>(p_stage(it, 0) + po);
+        const VT cc = *reinterpret_cast<const VT*>(p_stage(it, 1) + po);
+        const VT ec = *reinterpret_cast<const VT*>(p_stage(it, 2) + po);
+        VT res;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            const T rhs = A::add(A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1])),
+                                 A::mul(ly[e], a.ih[2]));
+            res.e[e] = time_update<T, EXACT>(rhs, q[R].e[e], cc.e[e], pc.e[e], ec.e[e], a.dt);
+        }
+        // null-Dirichlet face nodes are forced to +0 (kernel.hpp:87-88)
+        if ((zlo && z == 0 && a.gf[0][0] < 0) || (zhi && z == nz - 1 && a.gf[0][1] < 0)) {
+#pragma unroll
+            for (int e = 0; e < V; ++e) res.e[e] = T(0);
+        }
+        if (edge_tile) {
+            const bool dx = (pxl && x == 0 && a.gf[1][0] < 0) || (pxh && x == nx - 1 && a.gf[1][1] < 0);
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const int yy = y0 + e;
+                if (dx || (pyl && yy == 0 && a.gf[2][0] < 0) || (pyh && yy == ny - 1 && a.gf[2][1] < 0))
+                    res.e[e] = T(0);
+            }
+        }
+        if (xin) {
+            T* o = a.out + col0 + (long long)z * plane;
+            if (y0 + V <= ny) {
+                st16(o, res);
+            } else {
+#pragma unroll
+                for (int e = 0; e < V; ++e)
+                    if (y0 + e < ny) o[e] = res.e[e];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 2 * R; ++k) q[k] = q[k + 1];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// apply_boundary, kernel.hpp:67-102, as ONE launch per step.  Threads cover
+// every ghost cell of the level (global Z faces only for slabs; internal ghost
+// planes arrive by halo exchange) plus every node of an active null-Dirichlet
+// face.  A ghost cell takes prod(f_a) * u(m): m mirrors each ghost coordinate
+// about its face (f = -1 Dirichlet, +1 Neumann), 0 if any side is "none" or if
+// m lies on a Dirichlet face (that node is zeroed in the same pass).  This is
+// the closed form of the reference's axis-by-axis passes (values equal; only
+// the sign of a zero may differ in ghost cells, which never reaches an
+// extended point).
+struct BoxRegion {
+    int p0[3];      // first padded coordinate (z, x, y)
+    int n[3];       // extent
+    int zero_face;  // 1: Dirichlet face nodes (write 0); 0: ghost cells
+};
+
+struct BoundaryArgs {
+    int nd;
+    int h;
+    int ext[3];            // extended extents (local Z)
+    signed char f[3][2];   // -1 Dirichlet, +1 Neumann, 0 none
+    unsigned char act[3][2];
+    long long s[3];        // strides (plane, ld, 1) / 2D (ld, 1, 0)
+    long long origin_pad;  // offset of padded (0,0,0)
+    int n_regions;
+    BoxRegion reg[12];
+    long long start[13];   // prefix sums of region sizes
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) boundary_kernel(T* f, BoundaryArgs b, const Ctrl* ctrl) {
+    // blockIdx.y selects the region; blocks past its size exit
+    if (ctrl && ctrl->abort) return;
+    const BoxRegion& R = b.reg[blockIdx.y];
+    const int size = R.n[0] * R.n[1] * R.n[2];
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= size) return;
+    const int k2 = q % R.n[2];
+    const int r12 = q / R.n[2];
+    const int k1 = r12 % R.n[1];
+    const int k0 = r12 / R.n[1];
+    const int p0 = R.p0[0] + k0, p1 = R.p0[1] + k1, p2 = R.p0[2] + k2;
+    T* dst = f + b.origin_pad + (long long)p0 * b.s[0] + (long long)p1 * b.s[1] + (long long)p2 * b.s[2];
+    if (R.zero_face) {
+        *dst = T(0);
+        return;
+    }
+    int fac = 1;
+    bool on_dir = false;
+    long long src = b.origin_pad;
+    const int p[3] = {p0, p1, p2};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (a < b.nd) {
+            const int e = p[a] - b.h;  // extended coordinate
+            int m = e;
+            if (e < 0) {
+                m = -e;
+                fac *= b.f[a][0];
+            } else if (e >= b.ext[a]) {
+                m = 2 * (b.ext[a] - 1) - e;
+                fac *= b.f[a][1];
+            }
+            on_dir |= (b.act[a][0] && b.f[a][0] < 0 && m == 0) ||
+                      (b.act[a][1] && b.f[a][1] < 0 && m == b.ext[a] - 1);
+            src += (long long)(m + b.h) * b.s[a];
+        }
+    }
+    if (fac == 0 || on_dir) {
+        *dst = T(0);
+    } else {
+        const T v = f[src];
+        *dst = fac < 0 ? -v : v;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // inject, kernel.hpp:429-438.  One thread per distinct target index; its
 // entries are applied in the reference's (point, entry) order.
@@ -397,8 +655,7 @@ __global__ void inject_kernel(T* out, const T* __restrict__ c2dt2, const T* __re
                               double dt, const long long* __restrict__ tgt,
                               const unsigned int* __restrict__ ent_off,
                               const double* __restrict__ ent_w, const double* __restrict__ wavelet,
-                              unsigned long long n_wavelet, int n_tgt, int k, const Ctrl* ctrl,
-                              Faces F, long long origin, int R) {
+                              unsigned long long n_wavelet, int n_tgt, int k, const Ctrl* ctrl) {
     using A = Ar<T, true>;  // the reference's scalar order; never contracted
     if (ctrl->abort) return;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -415,29 +672,17 @@ __global__ void inject_kernel(T* out, const T* __restrict__ c2dt2, const T* __re
     for (unsigned int q = ent_off[t]; q < ent_off[t + 1]; ++q)
         val = A::add(val, A::mul(A::mul(c2, static_cast<T>(__dmul_rn(ent_w[q], amp))), iop));
     out[i] = val;
-    // refresh the ghost copies of this point (targets on Dirichlet faces were
-    // dropped on the host: apply_boundary zeroes them after injection)
-    const long long rem = i - origin;
-    int c[3];
-    if (F.nd == 3) {
-        c[0] = (int)(rem / F.s[0]);
-        c[1] = (int)((rem % F.s[0]) / F.s[1]);
-        c[2] = (int)(rem % F.s[1]);
-    } else {
-        c[0] = (int)(rem / F.s[0]);
-        c[1] = (int)(rem % F.s[0]);
-        c[2] = 0;
-    }
-    if (near_face(F, c, R)) ghost_writes(out, i, c, val, F, R);
 }
 
 // apply_boundary, kernel.hpp:67-102, one axis per launch (the reference's axis
 // order is kept by launching axis 0, 1, 2 in sequence).  One thread per line.
+// mode: 0 always, 1 skip when aborted, 2 only when a non-finite value was found
 template <typename T>
 __global__ void ghost_lines(T* f, long long origin_pad, long long sa, int n_ext, int h,
                             long long s1, int n1, long long s2, int n2, int bc_lo, int bc_hi,
-                            int do_lo, int do_hi, const Ctrl* ctrl) {
-    if (ctrl && ctrl->abort) return;
+                            int do_lo, int do_hi, const Ctrl* ctrl, int mode) {
+    if (mode == 1 && ctrl->abort) return;
+    if (mode == 2 && ctrl->bad_idx == ~0ull) return;
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (long long)n1 * n2) return;
     const int i2 = (int)(t % n2), i1 = (int)(t / n2);
@@ -479,10 +724,27 @@ __global__ void __launch_bounds__(32 * REC_WARPS)
     if (r >= n_rec || row >= n_rows) return;
     const unsigned int b = off[r], e = off[r + 1];
     double acc = 0.0;
+    constexpr int BATCH = 8;  // gathers in flight per lane
     for (unsigned int base = b; base < e; base += REC_CHUNK) {
         const int m = (int)min((unsigned int)REC_CHUNK, e - base);
-        for (int k = lane; k < m; k += 32)
-            prod[warp][k] = __dmul_rn(w[base + k], static_cast<double>(u[idx[base + k]]));
+        for (int k0 = 0; k0 < m; k0 += 32 * BATCH) {
+            long long ix[BATCH];
+            double wt[BATCH];
+            T uv[BATCH];
+#pragma unroll
+            for (int j = 0; j < BATCH; ++j) {
+                const int k = k0 + j * 32 + lane;
+                ix[j] = k < m ? idx[base + k] : idx[base];
+                wt[j] = k < m ? w[base + k] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < BATCH; ++j) uv[j] = u[ix[j]];
+#pragma unroll
+            for (int j = 0; j < BATCH; ++j) {
+                const int k = k0 + j * 32 + lane;
+                if (k < m) prod[warp][k] = __dmul_rn(wt[j], static_cast<double>(uv[j]));
+            }
+        }
         __syncwarp();
         if (lane == 0) {
 #pragma unroll 8
@@ -496,19 +758,24 @@ __global__ void __launch_bounds__(32 * REC_WARPS)
 // max_abs / check_health, kernel.hpp:265-273 and :456-458.  max |u| over
 // finite values plus the smallest global padded flat index holding a
 // non-finite value (the reference returns the first one in flat order).
+// Scans the box [p0, p0+n_planes) x [r0, r0+n_rows) x [c0, c0+n_cols) of padded
+// local coordinates; flat indices are GLOBAL padded (gplane0 = global padded
+// plane of local plane 0).  only_if_bad: run only after a non-finite was seen.
 template <typename T>
 __global__ void health_kernel(const T* __restrict__ u, long long origin_pad, long long ld,
-                              long long plane, int n_planes, int n_rows, int n_cols,
-                              unsigned long long gplane0, unsigned long long P1,
-                              unsigned long long P2, int is3d, Ctrl* ctrl, int honor_abort) {
+                              long long plane, int p0, int n_planes, int r0, int n_rows, int c0,
+                              int n_cols, unsigned long long gplane0, unsigned long long P1,
+                              unsigned long long P2, int is3d, Ctrl* ctrl, int honor_abort,
+                              int only_if_bad) {
     if (honor_abort && ctrl->abort) return;
+    if (only_if_bad && ctrl->bad_idx == ~0ull) return;
     double m = 0.0;
     unsigned long long bad = ~0ull;
     const long long total = (long long)n_planes * n_rows;
     for (long long pr = blockIdx.x; pr < total; pr += gridDim.x) {
-        const int p = (int)(pr / n_rows), r = (int)(pr % n_rows);
+        const int p = p0 + (int)(pr / n_rows), r = r0 + (int)(pr % n_rows);
         const T* row = u + origin_pad + (long long)p * plane + (long long)r * ld;
-        for (int c = threadIdx.x; c < n_cols; c += blockDim.x) {
+        for (int c = c0 + threadIdx.x; c < c0 + n_cols; c += blockDim.x) {
             const double av = fabs(static_cast<double>(row[c]));
             if (!isfinite(av)) {
                 const unsigned long long flat =

@@ -1,0 +1,69 @@
+"""Multi-GPU host plumbing for the Z-slab decomposition (one process per GPU).
+
+The library owns the data path (NCCL send/recv of R halo planes per internal
+face inside the step graph, fdw_api.cu launch_halo); this module only does the
+control-plane work around it with torch.distributed:
+  * broadcast the NCCL unique id from rank 0,
+  * build each rank's slab workload (configs.build_workload(rank, world)),
+  * reduce per-rank partial seismograms in rank order (double) and cast to T,
+  * gather halo-stripped slabs for checking.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+
+def nccl_unique_id(group=None) -> bytes:
+    """ncclGetUniqueId on rank 0, broadcast to every rank of `group`."""
+    import torch.distributed as dist
+    buf = (C.c_ubyte * 128)()
+    if dist.get_rank(group) == 0:
+        rc = _lib.lib().fdw_nccl_unique_id(C.byref(buf))
+        if rc != 0:
+            raise RuntimeError("ncclGetUniqueId failed")
+    obj = [bytes(buf)]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
+def slab_range(n_ext: int, world: int, rank: int) -> tuple:
+    b, e = C.c_uint64(), C.c_uint64()
+    if _lib.lib().fdw_slab_range(n_ext, world, rank, C.byref(b), C.byref(e)) != 0:
+        raise ValueError(f"cannot split {n_ext} planes over {world} ranks")
+    return int(b.value), int(e.value)
+
+
+def reduce_seismogram(partial: np.ndarray, dtype, group=None) -> np.ndarray:
+    """Sum of per-rank double partials in rank order (rank 0 first), cast to T.
+    For world == 1 this is the reference's own accumulation (acquisition.hpp:
+    155-158); for world > 1 the per-receiver sum is split at slab faces."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = torch.from_numpy(np.ascontiguousarray(partial, np.float64))
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    acc = parts[0].numpy().copy()
+    for p in parts[1:]:
+        acc += p.numpy()
+    return acc.astype(dtype)
+
+
+def gather_slabs(local_ext: np.ndarray, group=None) -> np.ndarray:
+    """Concatenate halo-stripped local slabs along Z (rank order) on every rank."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = torch.from_numpy(np.ascontiguousarray(local_ext))
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([t.shape[0]]), group=group)
+    mx = int(max(s.item() for s in sizes))
+    pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype)
+    pad[: t.shape[0]] = t
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return np.concatenate([p[: int(s.item())].numpy() for p, s in zip(parts, sizes)], axis=0)

@@ -391,7 +391,8 @@ class Solver:
         _lib.lib().fdw_layout(self._ctx, C.byref(ld), C.byref(plane), C.byref(base), C.byref(planes),
                               C.byref(var))
         return {"ld": ld.value, "plane": plane.value, "base": base.value, "planes": planes.value,
-                "variant": var.value & 0xFF, "z_segments": var.value >> 8}
+                "variant": var.value & 0xFF, "z_segments": (var.value >> 8) & 0xFF,
+                "ctas_per_sm": var.value >> 16}
 
     def set_stream(self, stream_ptr: int):
         _check(self._ctx, _lib.lib().fdw_set_stream(self._ctx, C.c_void_p(stream_ptr)), "fdw_set_stream")

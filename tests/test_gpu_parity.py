@@ -9,7 +9,7 @@ import pytest
 
 from helpers import D, N, X, gpu_solver, oracle_solver, rel_l2, run_both, same, small_config
 from paper_2201_05278_b200 import InstabilityError
-from paper_2201_05278_b200._lib import (FDW_KERNEL_SIMPLE, FDW_KERNEL_ZMARCH, FDW_MATH_FMA)
+from paper_2201_05278_b200._lib import (FDW_KERNEL_SIMPLE, FDW_KERNEL_TMA, FDW_KERNEL_ZMARCH, FDW_MATH_FMA)
 from paper_2201_05278_b200.configs import build_workload
 
 pytestmark = pytest.mark.gpu
@@ -37,7 +37,7 @@ def test_2d_exact(order, dtype, bci):
 
 @pytest.mark.parametrize("order", [2, 4, 6, 8])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("variant", [FDW_KERNEL_SIMPLE, FDW_KERNEL_ZMARCH])
+@pytest.mark.parametrize("variant", [FDW_KERNEL_SIMPLE, FDW_KERNEL_ZMARCH, FDW_KERNEL_TMA])
 @pytest.mark.parametrize("bci", range(3))
 def test_3d_exact(order, dtype, variant, bci):
     cfg = small_config(ndim=3, order=order, shape=(17, 27, 21), damping_cells=4, bc=BCS[bci], tf=0.12)
@@ -51,10 +51,11 @@ def test_3d_exact(order, dtype, variant, bci):
 
 @pytest.mark.parametrize("shape", [(13, 33, 65), (29, 17, 69), (12, 49, 7), (40, 18, 131)])
 @pytest.mark.parametrize("zseg", [1, 3, 7])
-def test_3d_zmarch_ragged_tiles(shape, zseg):
+@pytest.mark.parametrize("variant", [FDW_KERNEL_ZMARCH, FDW_KERNEL_TMA])
+def test_3d_zmarch_ragged_tiles(shape, zseg, variant):
     """Partial Y vectors / X tiles / Z segments all cover the grid exactly once."""
     cfg = small_config(ndim=3, order=8, shape=shape, damping_cells=3, tf=0.06)
-    w, g, res, o, ref = run_both(cfg, np.float32, variant=FDW_KERNEL_ZMARCH, z_segments=zseg)
+    w, g, res, o, ref = run_both(cfg, np.float32, variant=variant, z_segments=zseg)
     assert same(res.seismogram.data, ref["seismogram"])
     assert same(res.snapshots[-1], ref["final"])
     assert same(g.current_level(), o.current())

@@ -5,27 +5,33 @@ import numpy as np
 from paper_2201_05278_b200 import configs, Solver, make_material_model, DampingField
 from paper_2201_05278_b200._lib import *
 
+_cache = {}
 def run(name, cfg, steps, **kw):
-    t = time.time()
-    w = configs.build_workload(cfg, np.float32)
-    tsetup = time.time() - t
+    key = cfg.name
+    if key not in _cache:
+        _cache.clear()
+        _cache[key] = configs.build_workload(cfg, np.float32)
+    w = _cache[key]
     s = Solver(w.grid, make_material_model(w.velocity), DampingField(eta=w.eta), w.spec, w.axis, w.coeffs, **kw)
     s.set_sources(w.sources, w.wavelet); s.set_receivers(w.receivers)
-    s.advance_raw(100)  # warm (graph capture)
+    s.advance_raw(100, record=True)  # warm (graph capture)
     pts = w.grid.extended_points()
-    t = time.time(); s.advance_raw(steps); el = time.time() - t
+    t = time.time(); s.advance_raw(steps, record=True); el = time.time() - t
     ms = s.profile_steps(20)
-    out = dict(name=name, kw={k: int(v) for k, v in kw.items()}, layout=s.layout(), setup_s=round(tsetup, 2),
-               gpts=pts * steps / el / 1e9, ms_step=el / steps * 1e3, prof_ms=[round(x, 4) for x in ms],
-               sweep_gbs=pts * 20 / (ms[0] * 1e-3) / 1e9)
+    out = dict(name=name, kw={k: int(v) for k, v in kw.items()}, layout=s.layout(),
+               gpts=round(pts * steps / el / 1e9, 2), ms_step=round(el / steps * 1e3, 4), prof_ms=[round(x, 4) for x in ms],
+               sweep_gbs=round(pts * 20 / (ms[0] * 1e-3) / 1e9, 1))
     print(json.dumps(out), flush=True)
     s.close()
 
-run("C4", configs.overthrust3d(8), 400)
-run("C4-simple", configs.overthrust3d(8), 200, variant=FDW_KERNEL_SIMPLE)
-run("C4-fma", configs.overthrust3d(8), 400, math=FDW_MATH_FMA)
-for zs in (1, 2, 3, 4):
-    run(f"C4-zseg{zs}", configs.overthrust3d(8), 200, z_segments=zs)
-run("C3", configs.overthrust3d(4), 400)
-run("C2", configs.marmousi2d(8), 1600)
-run("C1", configs.marmousi2d(2), 1300)
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["all"]
+    c4 = configs.overthrust3d(8)
+    run("C4-tma", c4, 400)
+    run("C4-zmarch", c4, 400, variant=FDW_KERNEL_ZMARCH)
+    run("C4-tma-fma", c4, 400, math=FDW_MATH_FMA)
+    for zs in (2, 3, 4, 6, 8):
+        run(f"C4-tma-zseg{zs}", c4, 200, z_segments=zs)
+    run("C3-tma", configs.overthrust3d(4), 400)
+    run("C2", configs.marmousi2d(8), 1600)
+    run("C1", configs.marmousi2d(2), 1300)
