@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfdwave_cuda.so")
+LIB_PATH = os.environ.get("FDW_LIB") or os.path.join(_HERE, "libfdwave_cuda.so")  # FDW_LIB: A/B builds
 
 FDW_ABI_VERSION = 1
 FDW_OK, FDW_EINVAL, FDW_ECUDA, FDW_ENCCL, FDW_EINSTABLE, FDW_ENOMEM, FDW_ESTATE = range(7)

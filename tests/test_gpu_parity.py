@@ -9,7 +9,8 @@ import pytest
 
 from helpers import D, N, X, gpu_solver, oracle_solver, rel_l2, run_both, same, small_config
 from paper_2201_05278_b200 import InstabilityError
-from paper_2201_05278_b200._lib import (FDW_KERNEL_SIMPLE, FDW_KERNEL_TMA, FDW_KERNEL_ZMARCH, FDW_MATH_FMA)
+from paper_2201_05278_b200._lib import (FDW_KERNEL_SIMPLE, FDW_KERNEL_TMA, FDW_KERNEL_ZMARCH,
+                                        FDW_MATH_FMA)
 from paper_2201_05278_b200.configs import build_workload
 
 pytestmark = pytest.mark.gpu
