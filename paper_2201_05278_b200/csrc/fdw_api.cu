@@ -1044,9 +1044,20 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
     };
     if (!ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream")) return bail(FDW_ECUDA);
     c->own_stream = true;
+    // The four field arrays come from the device's stream-ordered pool with an
+    // unlimited release threshold: a process that builds one Solver after
+    // another (the reference's one-run-per-Solver usage) reuses the
+    // same physical pages instead of paying cudaMalloc/cudaFree each time.
     const size_t bytes = c->level_elems * c->tsize;
+    {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, d.device) == cudaSuccess) {
+            unsigned long long thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     for (void** p : {&c->lvl[0], &c->lvl[1], &c->c2dt2, &c->eta}) {
-        if (!ck(cudaMalloc(p, bytes), "cudaMalloc(level)")) return bail(FDW_ENOMEM);
+        if (!ck(cudaMallocAsync(p, bytes, c->stream), "cudaMallocAsync(level)")) return bail(FDW_ENOMEM);
         if (!ck(cudaMemsetAsync(*p, 0, bytes, c->stream), "memset")) return bail(FDW_ECUDA);
     }
     if (!ck(cudaMalloc(&c->ctrl, sizeof(Ctrl)), "cudaMalloc(ctrl)")) return bail(FDW_ENOMEM);
@@ -1114,9 +1125,11 @@ fdw_status fdw_destroy(fdw_solver* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     if (c->comm) ncclCommDestroy(c->comm);
-    for (void* p : {c->lvl[0], c->lvl[1], c->c2dt2, c->eta, (void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off,
-                    (void*)c->d_ent_w, (void*)c->d_wavelet, (void*)c->d_rec_idx, (void*)c->d_rec_off,
-                    (void*)c->d_rec_w, (void*)c->d_seis})
+    for (void* p : {c->lvl[0], c->lvl[1], c->c2dt2, c->eta})
+        if (p) cudaFreeAsync(p, c->stream);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (void* p : {(void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off, (void*)c->d_ent_w, (void*)c->d_wavelet,
+                    (void*)c->d_rec_idx, (void*)c->d_rec_off, (void*)c->d_rec_w, (void*)c->d_seis})
         if (p) cudaFree(p);
     if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -196,6 +196,12 @@ class Solver:
         self._prev = None
         self._curr = None
         self._host_view = False
+        self._alloc = np.empty
+
+    def set_host_allocator(self, fn):
+        """fn(shape, dtype) -> ndarray used for forward() results (snapshots,
+        seismogram); pass a pinned-memory allocator for full-speed D2H."""
+        self._alloc = fn or np.empty
 
     # -- lifetime --
     def close(self):
@@ -351,7 +357,7 @@ class Solver:
         _check(self._ctx, L.fdw_synchronize(self._ctx), "fdw_synchronize")
         res.kernel_seconds = time.perf_counter() - t0
         if self._n_rec:
-            data = np.empty((n_total + 1) * self._n_rec, self._dtype)
+            data = self._alloc(((n_total + 1) * self._n_rec,), self._dtype)
             _check(self._ctx, L.fdw_download_seismogram(self._ctx, ptr(data), n_total + 1),
                    "fdw_download_seismogram")
             res.seismogram.data = data
@@ -360,7 +366,7 @@ class Solver:
         return res
 
     def _snapshot(self, res, step):
-        out = np.empty(tuple(self._grid.extended_shape[:self._grid.ndim]), self._dtype)
+        out = self._alloc(tuple(self._extended_local()), self._dtype)
         _check(self._ctx, _lib.lib().fdw_get_extended(self._ctx, ptr(out)), "fdw_get_extended")
         res.snapshots.append(out)
         res.snapshot_steps.append(step)
@@ -380,8 +386,14 @@ class Solver:
                "fdw_download_seismogram_f64")
         return out
 
+    def _extended_local(self):
+        ext = list(self._grid.extended_shape[:self._grid.ndim])
+        if self._desc.world > 1:
+            ext[0] = int(self._desc.z_end - self._desc.z_begin)
+        return ext
+
     def extended_level(self) -> np.ndarray:
-        out = np.empty(tuple(self._grid.extended_shape[:self._grid.ndim]), self._dtype)
+        out = np.empty(tuple(self._extended_local()), self._dtype)
         _check(self._ctx, _lib.lib().fdw_get_extended(self._ctx, ptr(out)), "fdw_get_extended")
         return out
 
