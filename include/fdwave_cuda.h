@@ -54,7 +54,8 @@ enum {
     FDW_KERNEL_AUTO = 0,   /* best registered kernel for (ndim, order, dtype) */
     FDW_KERNEL_SIMPLE = 1, /* one thread per point, cache-fed (parity baseline) */
     FDW_KERNEL_ZMARCH = 2, /* 3D: 2.5D Z-march, smem X-Y plane + register Z queue (LDG-fed) */
-    FDW_KERNEL_TMA = 3     /* 3D: Z-march fed by cp.async.bulk.tensor (TMA) + mbarrier rings */
+    FDW_KERNEL_TMA = 3,    /* 3D: Z-march fed by cp.async.bulk.tensor (TMA) + mbarrier rings */
+    FDW_KERNEL_FUSED2D = 4 /* 2D: persistent cooperative kernel, one grid barrier per time step */
 };
 
 /* Arithmetic mode (fdw_desc.math). */

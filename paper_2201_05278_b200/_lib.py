@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("FDW_LIB") or os.path.join(_HERE, "libfdwave_cuda.so")
 
 FDW_ABI_VERSION = 1
 FDW_OK, FDW_EINVAL, FDW_ECUDA, FDW_ENCCL, FDW_EINSTABLE, FDW_ENOMEM, FDW_ESTATE = range(7)
-FDW_KERNEL_AUTO, FDW_KERNEL_SIMPLE, FDW_KERNEL_ZMARCH, FDW_KERNEL_TMA = 0, 1, 2, 3
+FDW_KERNEL_AUTO, FDW_KERNEL_SIMPLE, FDW_KERNEL_ZMARCH, FDW_KERNEL_TMA, FDW_KERNEL_FUSED2D = 0, 1, 2, 3, 4
 FDW_MATH_EXACT, FDW_MATH_FMA = 0, 1
 FDW_ADVANCE_RECORD = 1
 

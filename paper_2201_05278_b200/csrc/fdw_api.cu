@@ -98,6 +98,8 @@ struct fdw_solver {
     // TMA descriptors (variant FDW_KERNEL_TMA): u-tile box for each level, and
     // the prev/c2dt2/eta tile box for each level, c2dt2 and eta
     CUtensorMap tm_u[2], tm_p[2], tm_c, tm_e;
+    int* d_tmap = nullptr;       // FUSED2D: dense injection-target map over the extended grid
+    int fused_grid = 0;          // FUSED2D: co-resident blocks of the cooperative kernel
 };
 
 namespace {
@@ -365,6 +367,72 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a, int src, int dst) {
 #undef LT
         default: return false;
     }
+}
+
+template <typename T, bool EX>
+const void* fused2d_fn(int R) {
+#define F2(RR) \
+    if (R == RR) return (const void*)fdw::step2d_fused<T, RR, EX>;
+    F2(1) F2(2) F2(3) F2(4) F2(5) F2(6) F2(7) F2(8) F2(9) F2(10)
+#undef F2
+    return nullptr;
+}
+
+template <typename T>
+const void* fused2d_kernel(int R, bool ex) {
+    return ex ? fused2d_fn<T, true>(R) : fused2d_fn<T, false>(R);
+}
+
+template <typename T>
+fdw_status launch_fused2d_t(fdw_solver* c, int L, int cur0, bool record, int k0) {
+    fdw::Fused2DArgs<T> a{};
+    a.lvl[0] = static_cast<T*>(c->lvl[0]);
+    a.lvl[1] = static_cast<T*>(c->lvl[1]);
+    a.c2dt2 = static_cast<const T*>(c->c2dt2);
+    a.eta = static_cast<const T*>(c->eta);
+    for (int j = 0; j <= c->R; ++j) a.v[j] = static_cast<T>(c->d.coeffs[j]);
+    for (int k = 0; k < 2; ++k) a.ih[k] = static_cast<T>(1.0 / (c->d.spacing[k] * c->d.spacing[k]));
+    a.ih[2] = T(1);
+    a.dt = c->d.dt;
+    a.ld = c->ld;
+    a.origin = c->origin;
+    a.nz = (int)c->nzl;
+    a.nx = (int)c->nxl;
+    for (int ax = 0; ax < 2; ++ax)
+        for (int sd = 0; sd < 2; ++sd) {
+            const int bc = c->d.bc[ax][sd];
+            a.gf[ax][sd] = bc == FDW_BC_NULL_DIRICHLET ? -1 : bc == FDW_BC_NULL_NEUMANN ? 1 : 0;
+        }
+    a.tmap = c->d_tmap;
+    a.ent_off = c->d_ent_off;
+    a.ent_w = c->d_ent_w;
+    a.wavelet = c->d_wavelet;
+    a.n_wavelet = c->n_wavelet;
+    a.ridx = c->d_rec_idx;
+    a.roff = c->d_rec_off;
+    a.rw = c->d_rec_w;
+    a.seis = c->d_seis;
+    a.n_rec = c->d_seis ? c->n_rec : 0;
+    a.n_rows = c->seis_rows;
+    a.ctrl = c->ctrl;
+    {
+        const char* dbg = std::getenv("FDW_DEBUG_FUSED");
+        a.dbg = dbg ? std::atoi(dbg) : 0;
+    }
+    int rec = record && c->d_seis ? 1 : 0;
+    void* args[] = {&a, &L, &cur0, &rec, &k0};
+    const void* f = fused2d_kernel<T>(c->R, c->d.math == FDW_MATH_EXACT);
+    CU(cudaLaunchCooperativeKernel(f, dim3((unsigned)c->fused_grid), dim3(256), args, 0, c->stream));
+    if (c->capturing)
+        ++c->capture_kernels;
+    else
+        ++c->launches;
+    return FDW_OK;
+}
+
+fdw_status launch_fused2d(fdw_solver* c, int L, int cur0, bool record, int k0) {
+    return c->tsize == 4 ? launch_fused2d_t<float>(c, L, cur0, record, k0)
+                         : launch_fused2d_t<double>(c, L, cur0, record, k0);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -675,6 +743,8 @@ struct Mark {
 // Virtual-ghost path for a step reading level `src`: only the TMA kernel, and
 // only when src's stored ghosts are not caller-provided raw values.
 bool virtual_step(const fdw_solver* c, int gstate_src) {
+    // FUSED2D reads stored ghosts (any state) and leaves corner ghosts stale
+    if (c->variant == FDW_KERNEL_FUSED2D) return true;
     return c->variant == FDW_KERNEL_TMA && gstate_src != 2;
 }
 
@@ -693,8 +763,23 @@ fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
 fdw_status enqueue_chunk(fdw_solver* c, unsigned long long L, int cur0, bool check, bool record, bool first_virt,
                          bool rest_virt) {
     fdw_status s;
-    for (unsigned long long k = 0; k < L; ++k)
-        if ((s = enqueue_step(c, (int)k, cur0 ^ (int)(k & 1), record, k == 0 ? first_virt : rest_virt))) return s;
+    if (c->variant == FDW_KERNEL_FUSED2D) {
+        // one cooperative launch for the chunk (one per step when profiling);
+        // a raw first level takes one stored-ghost step first
+        unsigned long long k0 = 0;
+        (void)first_virt;  // stored ghosts: a raw (caller-uploaded) level is read as stored
+        if (c->prof) {
+            for (unsigned long long k = k0; k < L; ++k) {
+                Mark m(c, 0);
+                if ((s = launch_fused2d(c, 1, cur0 ^ (int)(k & 1), record, (int)k))) return s;
+            }
+        } else if (L > k0) {
+            if ((s = launch_fused2d(c, (int)(L - k0), cur0 ^ (int)(k0 & 1), record, (int)k0))) return s;
+        }
+    } else {
+        for (unsigned long long k = 0; k < L; ++k)
+            if ((s = enqueue_step(c, (int)k, cur0 ^ (int)(k & 1), record, k == 0 ? first_virt : rest_virt))) return s;
+    }
     fdw::step_advance<<<1, 1, 0, c->stream>>>(c->ctrl, L);
     CHECK_LAUNCH();
     if (check) {
@@ -711,7 +796,7 @@ fdw_status run_chunk(fdw_solver* c, unsigned long long L, bool check, bool recor
     const int cur0 = c->cur;
     const bool first_virt = virtual_step(c, c->gstate[cur0]);
     const bool rest_virt = virtual_step(c, 0);
-    if (L < 8 || c->prof) {
+    if (L < 8 || c->prof || c->variant == FDW_KERNEL_FUSED2D) {
         fdw_status s = enqueue_chunk(c, L, cur0, check, record, first_virt, rest_virt);
         if (s) return s;
     } else {
@@ -1067,7 +1152,21 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
     // kernel selection
     int variant = d.variant;
     if (variant == FDW_KERNEL_AUTO)
-        variant = (c->ndim == 3 && zmarch_supported(R)) ? FDW_KERNEL_TMA : FDW_KERNEL_SIMPLE;
+        variant = c->ndim == 2 ? FDW_KERNEL_FUSED2D
+                               : (zmarch_supported(R) ? FDW_KERNEL_TMA : FDW_KERNEL_SIMPLE);
+    if (variant == FDW_KERNEL_FUSED2D && c->ndim != 2) variant = FDW_KERNEL_SIMPLE;
+    if (variant == FDW_KERNEL_FUSED2D) {
+        const bool ex = d.math == FDW_MATH_EXACT;
+        const void* f = c->tsize == 4 ? fused2d_kernel<float>(R, ex) : fused2d_kernel<double>(R, ex);
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 256, 0) != cudaSuccess || occ < 1) occ = 1;
+        const long long need = (c->nzl * c->nxl + 255) / 256;
+        c->fused_grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)occ * c->sm_count));
+        c->occupancy = occ;
+        const size_t n = (size_t)(c->nzl * c->nxl) * sizeof(int);
+        if (!ck(cudaMalloc(&c->d_tmap, n), "cudaMalloc(tmap)")) return bail(FDW_ENOMEM);
+        if (!ck(cudaMemsetAsync(c->d_tmap, 0, n, c->stream), "memset(tmap)")) return bail(FDW_ECUDA);
+    }
     if ((variant == FDW_KERNEL_ZMARCH || variant == FDW_KERNEL_TMA) && (c->ndim != 3 || !zmarch_supported(R)))
         variant = FDW_KERNEL_SIMPLE;
     if (variant == FDW_KERNEL_TMA) {
@@ -1129,7 +1228,7 @@ fdw_status fdw_destroy(fdw_solver* c) {
         if (p) cudaFreeAsync(p, c->stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void* p : {(void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off, (void*)c->d_ent_w, (void*)c->d_wavelet,
-                    (void*)c->d_rec_idx, (void*)c->d_rec_off, (void*)c->d_rec_w, (void*)c->d_seis})
+                    (void*)c->d_rec_idx, (void*)c->d_rec_off, (void*)c->d_rec_w, (void*)c->d_seis, (void*)c->d_tmap})
         if (p) cudaFree(p);
     if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -1207,6 +1306,16 @@ fdw_status fdw_set_sources(fdw_solver* c, uint64_t n_points, const uint64_t* off
     if ((s = dev_upload(c, &c->d_wavelet, wv))) return s;
     c->n_wavelet = wv.size();
     c->n_tgt = (int)tgt.size();
+    if (c->d_tmap) {  // FUSED2D: dense map extended point -> target index + 1
+        std::vector<int> tm((size_t)(c->nzl * c->nxl), 0);
+        for (size_t t = 0; t < tgt.size(); ++t) {
+            const long long rem = tgt[t] - c->origin;
+            const long long z = rem / c->ld, x = rem % c->ld;
+            if (z >= 0 && z < c->nzl && x >= 0 && x < c->nxl) tm[(size_t)(z * c->nxl + x)] = (int)t + 1;
+        }
+        CU(cudaMemcpyAsync(c->d_tmap, tm.data(), tm.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+    }
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
     return FDW_OK;

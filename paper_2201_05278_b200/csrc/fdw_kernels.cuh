@@ -9,6 +9,7 @@
 // proj/CMakeLists.txt:7-19).  With EXACT = false the compiler may contract.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -569,6 +570,182 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX>::THREADS, MINB)
 #pragma unroll
         for (int k = 0; k < 2 * R; ++k) q[k] = q[k + 1];
     }
+}
+
+// ---------------------------------------------------------------------------
+// 2D: one persistent cooperative kernel runs a whole chunk of time steps
+// (FDW_KERNEL_FUSED2D).  The 2D working set (C2: 3 MB per field) lives in L2,
+// so a step is launch/latency-bound; here a step is one grid-wide barrier:
+//   phase k: sweep of step k (virtual ghosts, Dirichlet faces forced to +0,
+//            point-source injection fused per target point) + the receiver
+//            row of step k-1 (its level is read-only during step k)
+//   grid.sync()
+// Loads of data written inside the launch use ld.global.cg (L2, no stale L1).
+template <typename T>
+struct Fused2DArgs {
+    T* lvl[2];
+    const T* __restrict__ c2dt2;
+    const T* __restrict__ eta;
+    T v[11];
+    T ih[3];
+    double dt;
+    long long ld, origin;
+    int nz, nx;
+    int gf[2][2];                // mirror factor per face: -1 Dirichlet, +1 Neumann, 0 none
+    const int* tmap;             // [nz*nx] injection target index + 1, 0 if none
+    const long long* tgt;        // unused here (offsets of targets)
+    const unsigned* ent_off;
+    const double* ent_w;
+    const double* wavelet;
+    unsigned long long n_wavelet;
+    const long long* ridx;       // receivers (device offsets), CSR
+    const unsigned* roff;
+    const double* rw;
+    double* seis;
+    int n_rec;
+    unsigned long long n_rows;
+    int dbg;                     // development: bit0 skip sweep, bit1 skip receivers
+    Ctrl* ctrl;
+};
+
+template <typename T>
+__device__ __forceinline__ T ldcg(const T* p) {
+    return __ldcg(p);
+}
+
+// Receiver rows inside the fused kernel: a warp per receiver, lanes form the
+// products into shared memory, lane 0 sums them in entry order (exact).
+constexpr int F2D_CHUNK = 128;
+template <typename T>
+__device__ void fused2d_receivers(const Fused2DArgs<T>& a, const T* u, unsigned long long row, int gwarp, int nwarps,
+                                  int lane, double* prod) {
+    if (row >= a.n_rows) return;
+    for (int r = gwarp; r < a.n_rec; r += nwarps) {
+        const unsigned b = a.roff[r], e = a.roff[r + 1];
+        double acc = 0.0;
+        for (unsigned base = b; base < e; base += F2D_CHUNK) {
+            const int m = (int)min((unsigned)F2D_CHUNK, e - base);
+#pragma unroll
+            for (int q = 0; q < F2D_CHUNK / 32; ++q) {
+                const int k = q * 32 + lane;
+                if (k < m) prod[k] = __dmul_rn(a.rw[base + k], static_cast<double>(u[a.ridx[base + k]]));
+            }
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll 8
+                for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, prod[k]);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) a.seis[row * (unsigned long long)a.n_rec + r] = acc;
+    }
+}
+
+template <typename T, int R, bool EXACT>
+__global__ void __launch_bounds__(256) step2d_fused(Fused2DArgs<T> a, int L, int cur0, int record, int k0) {
+    using A = Ar<T, EXACT>;
+    constexpr int V = 16 / sizeof(T);
+    constexpr int HY = ((R + V - 1) / V) * V;  // X window halo, whole vectors
+    constexpr int HV = HY / V;
+    using VT = Vec<T, V>;
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    if (a.ctrl->abort) return;  // same value in every block: nothing here writes it
+    // k0: steps of this chunk already taken before the launch (host-side split)
+    const unsigned long long base = a.ctrl->step + (unsigned long long)k0, row_base = a.ctrl->row_base;
+    const int nz = a.nz, nx = a.nx;
+    const int nxv = (nx + V - 1) / V;  // vectors per row
+    const int nitems = nz * nxv;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nth = gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31, gwarp = tid >> 5, nwarps = nth >> 5;
+    const long long ld = a.ld;
+    __shared__ double rec_prod[8][F2D_CHUNK];  // per warp (256 threads)
+    double* prod = rec_prod[threadIdx.x >> 5];
+    // Ghost cells are STORED: the thread that produces a point within R of a
+    // face also writes its mirror copies into the new level (apply_boundary,
+    // kernel.hpp:84-97: Dirichlet -u, Neumann +u, none 0), so every item reads
+    // plain 16-byte vectors.  grid.sync() ends with an L1 invalidate
+    // (CCTL.IVALL): cached loads never see a stale line of an earlier step.
+    for (int k = 0; k < L; ++k) {
+        const T* u = a.lvl[cur0 ^ (k & 1)];
+        T* out = a.lvl[1 ^ cur0 ^ (k & 1)];
+        const unsigned long long n = base + (unsigned long long)k;
+        for (int item = tid; item < ((a.dbg & 1) ? 0 : nitems); item += nth) {
+            const int z = item / nxv;
+            const int x0 = (item - z * nxv) * V;
+            const long long i0 = a.origin + (long long)z * ld + x0;
+            const VT c = *reinterpret_cast<const VT*>(u + i0);
+            T lz[V], lx[V], res[V];
+#pragma unroll
+            for (int e = 0; e < V; ++e) lz[e] = lx[e] = A::mul(a.v[0], c.e[e]);
+            T w[2 * HY + V];
+#pragma unroll
+            for (int q = 0; q < 2 * HV + 1; ++q) {
+                const VT t = *reinterpret_cast<const VT*>(u + i0 - HY + q * V);
+#pragma unroll
+                for (int e = 0; e < V; ++e) w[q * V + e] = t.e[e];
+            }
+#pragma unroll
+            for (int j = 1; j <= R; ++j) {
+                const VT zp = *reinterpret_cast<const VT*>(u + i0 + j * ld);
+                const VT zm = *reinterpret_cast<const VT*>(u + i0 - j * ld);
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    lz[e] = A::add(lz[e], A::mul(a.v[j], A::add(zp.e[e], zm.e[e])));
+                    lx[e] = A::add(lx[e], A::mul(a.v[j], A::add(w[HY + e + j], w[HY + e - j])));
+                }
+            }
+            const VT pv = *reinterpret_cast<const VT*>(out + i0);
+            const VT cv = ldg16(a.c2dt2 + i0);
+            const VT ev = ldg16(a.eta + i0);
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const T rhs = A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1]));
+                res[e] = time_update<T, EXACT>(rhs, c.e[e], cv.e[e], pv.e[e], ev.e[e], a.dt);
+            }
+            const bool near = z <= R || z >= nz - 1 - R || x0 <= R || x0 + V - 1 >= nx - 1 - R;
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const int x = x0 + e;
+                if (x >= nx) break;
+                const int t = a.tmap[z * nx + x];
+                if (t) {  // inject, kernel.hpp:429-438 (entries in the reference's order)
+                    using AX = Ar<T, true>;
+                    const double amp = n < a.n_wavelet ? a.wavelet[n] : 0.0;
+                    T om, iop = T(1);
+                    if (ev.e[e] != T(0)) damping_factors(ev.e[e], a.dt, om, iop);
+                    for (unsigned q = a.ent_off[t - 1]; q < a.ent_off[t]; ++q)
+                        res[e] = AX::add(res[e], AX::mul(AX::mul(cv.e[e], static_cast<T>(__dmul_rn(a.ent_w[q], amp))), iop));
+                }
+                if (near) {
+                    if ((z == 0 && a.gf[0][0] < 0) || (z == nz - 1 && a.gf[0][1] < 0) || (x == 0 && a.gf[1][0] < 0) ||
+                        (x == nx - 1 && a.gf[1][1] < 0))
+                        res[e] = T(0);
+                    auto put = [&](int zz, int xx, int f) {
+                        out[a.origin + (long long)zz * ld + xx] = f == 0 ? T(0) : (f < 0 ? -res[e] : res[e]);
+                    };
+                    if (z >= 1 && z <= R) put(-z, x, a.gf[0][0]);
+                    if (z >= nz - 1 - R && z <= nz - 2) put(2 * (nz - 1) - z, x, a.gf[0][1]);
+                    if (x >= 1 && x <= R) put(z, -x, a.gf[1][0]);
+                    if (x >= nx - 1 - R && x <= nx - 2) put(z, 2 * (nx - 1) - x, a.gf[1][1]);
+                }
+            }
+            if (x0 + V <= nx) {
+                VT rv;
+#pragma unroll
+                for (int e = 0; e < V; ++e) rv.e[e] = res[e];
+                st16(out + i0, rv);
+            } else {
+                for (int e = 0; e < V && x0 + e < nx; ++e) out[i0 + e] = res[e];
+            }
+        }
+        if (record && k > 0 && !(a.dbg & 2))
+            fused2d_receivers(a, u, base + (unsigned long long)k - row_base, gwarp, nwarps, lane, prod);
+        grid.sync();
+    }
+    if (record)
+        fused2d_receivers(a, a.lvl[cur0 ^ (L & 1)], base + (unsigned long long)L - row_base, gwarp, nwarps, lane, prod);
 }
 
 // ---------------------------------------------------------------------------

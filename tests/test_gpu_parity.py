@@ -9,7 +9,7 @@ import pytest
 
 from helpers import D, N, X, gpu_solver, oracle_solver, rel_l2, run_both, same, small_config
 from paper_2201_05278_b200 import InstabilityError
-from paper_2201_05278_b200._lib import (FDW_KERNEL_SIMPLE, FDW_KERNEL_TMA, FDW_KERNEL_ZMARCH,
+from paper_2201_05278_b200._lib import (FDW_KERNEL_FUSED2D, FDW_KERNEL_SIMPLE, FDW_KERNEL_TMA, FDW_KERNEL_ZMARCH,
                                         FDW_MATH_FMA)
 from paper_2201_05278_b200.configs import build_workload
 
@@ -25,9 +25,10 @@ BCS = [
 @pytest.mark.parametrize("order", [2, 4, 8, 12, 20])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("bci", range(3))
-def test_2d_exact(order, dtype, bci):
+@pytest.mark.parametrize("variant", [FDW_KERNEL_SIMPLE, FDW_KERNEL_FUSED2D])
+def test_2d_exact(order, dtype, bci, variant):
     cfg = small_config(ndim=2, order=order, shape=(37, 53), damping_cells=6, bc=BCS[bci], tf=0.25)
-    w, g, res, o, ref = run_both(cfg, dtype)
+    w, g, res, o, ref = run_both(cfg, dtype, variant=variant)
     assert w.axis.n_steps > 20
     assert same(res.seismogram.data, ref["seismogram"])
     assert same(res.snapshots[-1], ref["final"])
@@ -74,6 +75,8 @@ def test_fma_mode_within_tolerance(ndim):
 @pytest.mark.parametrize("ndim", [2, 3])
 @pytest.mark.parametrize("bci", range(3))
 def test_step_api_random_levels(ndim, bci):
+    """(default variants: FUSED2D in 2D, TMA in 3D -- both take the stored-ghost
+    path for the first step after an upload)"""
     """Host-mirror semantics: write both levels, refresh, step -- levels equal
     the oracle's (ghosts included) after every step."""
     shape = (21, 25) if ndim == 2 else (14, 17, 19)

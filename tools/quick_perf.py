@@ -27,6 +27,13 @@ def run(name, cfg, steps, **kw):
 if __name__ == "__main__":
     which = sys.argv[1:] or ["all"]
     c4 = configs.overthrust3d(8)
+    if "2d" in which:
+        run("C2", configs.marmousi2d(8), 1600)
+        c2 = configs.marmousi2d(8); c2.alpha = 0.0
+        run("C2-alpha0", c2, 1600)
+        run("C2-simple", configs.marmousi2d(8), 1600, variant=FDW_KERNEL_SIMPLE)
+        run("C2-simple-alpha0", c2, 1600, variant=FDW_KERNEL_SIMPLE)
+        sys.exit(0)
     run("C4-tma", c4, 400)
     run("C4-zmarch", c4, 400, variant=FDW_KERNEL_ZMARCH)
     run("C4-tma-fma", c4, 400, math=FDW_MATH_FMA)
@@ -35,3 +42,4 @@ if __name__ == "__main__":
     run("C3-tma", configs.overthrust3d(4), 400)
     run("C2", configs.marmousi2d(8), 1600)
     run("C1", configs.marmousi2d(2), 1300)
+    run("C2-simple", configs.marmousi2d(8), 1600, variant=FDW_KERNEL_SIMPLE)
