@@ -2,7 +2,7 @@
 // /root/reference/proj/include/fdwave/kernel.hpp (lines 27-495).
 //
 // Put this directory BEFORE the reference include directory:
-//     g++ -std=c++20 -I<repo>/include -I<fdwave>/proj/include ... \
+//     g++ -std=c++20 -I<repo>/include -I<fdwave>/proj/include ...
 //         -L<repo>/paper_2201_05278_b200 -lfdwave_cuda
 // The reference headers' own  #include "fdwave/kernel.hpp"  then resolves here,
 // so runner.hpp, bench.hpp, verify.hpp and the reference tests compile
@@ -18,9 +18,10 @@
 // been handed out (the reference returns references to members, kernel.hpp:
 // 217-218, and its tests write initial conditions through them).
 //
-// Not on the CUDA path (throw std::invalid_argument, as SURVEY.md 8b
-// specifies): variable density (density_log_gradient is still provided on the
-// host) and add_volume_source.  set_backend is accepted and ignored.
+// Variable density (MaterialModel::density) runs on the GPU through
+// fdw_set_density (grad(rho)/rho formed on the device, kernel.hpp:104-136 and
+// :295-296).  Not on the CUDA path (throws std::invalid_argument, as SURVEY.md
+// 8b specifies): add_volume_source.  set_backend is accepted and ignored.
 #pragma once
 
 #include <array>
@@ -123,7 +124,7 @@ void apply_boundary(Field<T>& f, const Grid& grid, const BoundarySpec& spec) {
 }
 
 /// grad(rho)/rho per axis with the first-derivative stencil over the extended
-/// grid (host; kept for API parity -- the CUDA path is constant density).
+/// grid (host; API parity -- Solver<T> forms the same fields on the device).
 template <typename T>
 std::array<Field<T>, 3> density_log_gradient(const Field<T>& rho, const Grid& grid,
                                              const StencilCoeffs& coeffs) {
@@ -191,8 +192,6 @@ public:
         : grid_(std::move(grid)), boundary_(boundary), time_(time), coeffs_(std::move(coeffs)) {
         if (coeffs_.order != grid_.space_order)
             throw std::invalid_argument("stencil order does not match grid order");
-        if (materials.density)
-            throw std::invalid_argument("variable density is not supported on the CUDA path");
         fdw_desc d;
         fdw_desc_init(&d);
         d.ndim = grid_.ndim;
@@ -204,10 +203,21 @@ public:
             for (int side = 0; side < 2; ++side) d.bc[a][side] = static_cast<int32_t>(boundary_.face[a][side]);
         }
         for (std::size_t j = 0; j < coeffs_.second.size() && j < 11; ++j) d.coeffs[j] = coeffs_.second[j];
+        for (std::size_t j = 0; j < coeffs_.first.size() && j < 10; ++j) d.coeffs1[j] = coeffs_.first[j];
         d.dt = time_.dt;
         d.n_steps = time_.n_steps;
         check(fdw_create(&d, &ctx_), "fdw_create", true);
-        check(fdw_set_medium(ctx_, materials.velocity.data(), damping.eta.data(), 0), "fdw_set_medium");
+        try {
+            check(fdw_set_medium(ctx_, materials.velocity.data(), damping.eta.data(), 0), "fdw_set_medium");
+            if (materials.density) {
+                if (materials.density->size() != materials.velocity.size())
+                    throw std::invalid_argument("material model: density shape mismatch");
+                check(fdw_set_density(ctx_, materials.density->data(), 0), "fdw_set_density");
+            }
+        } catch (...) {
+            release();
+            throw;
+        }
         prev_ = Field<T>(grid_.ndim, grid_.padded_shape());
         curr_ = Field<T>(grid_.ndim, grid_.padded_shape());
     }

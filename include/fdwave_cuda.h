@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define FDW_ABI_VERSION 1
+#define FDW_ABI_VERSION 2
 
 typedef enum fdw_status {
     FDW_OK = 0,
@@ -90,6 +90,7 @@ typedef struct fdw_desc {
     uint64_t z_begin;        /* first extended Z plane owned by this rank */
     uint64_t z_end;          /* one past the last owned plane */
     unsigned char nccl_id[128]; /* ncclUniqueId from fdw_nccl_unique_id (world > 1) */
+    double coeffs1[10];      /* StencilCoeffs::first, w_1..w_r (variable density) stencil.hpp:96 */
 } fdw_desc;
 
 typedef struct fdw_solver fdw_solver;
@@ -114,6 +115,12 @@ fdw_status fdw_set_stream(fdw_solver* ctx, void* cuda_stream);
  * on_device = 1, device) padded slabs of T. */
 fdw_status fdw_set_medium(fdw_solver* ctx, const void* velocity, const void* eta,
                           int on_device);
+
+/* MaterialModel::density present -> the VariableDensity = true sweep
+ * (kernel.hpp:365-373 / :407-417).  grad(rho)/rho is formed on the device in
+ * double exactly as density_log_gradient (kernel.hpp:104-136); needs
+ * desc.coeffs1.  Padded slab of T (host, or device with on_device = 1). */
+fdw_status fdw_set_density(fdw_solver* ctx, const void* rho, int on_device);
 
 /* Solver<T>::set_sources, kernel.hpp:188-193: CSR view of an InterpolationMap
  * (offsets[n_points+1], idx/w[offsets[n_points]]) plus the wavelet (double,

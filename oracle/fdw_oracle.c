@@ -391,6 +391,8 @@ struct fdwo_solver {
     void* c2dt2;
     void* om;
     void* iop;
+    void* grad[3]; /* grad(rho)/rho per axis when variable density */
+    double w[10];  /* first-derivative coefficients w_1..w_r */
     /* sources / receivers: CSR */
     uint64_t n_src, n_rec;
     uint64_t *src_off, *src_idx, *rec_off, *rec_idx;
@@ -450,6 +452,7 @@ int fdwo_solver_create(const fdwo_grid* g, int dtype, const double* coeffs, doub
 
 void fdwo_solver_destroy(fdwo_solver* s) {
     if (!s) return;
+    for (int a = 0; a < 3; ++a) free(s->grad[a]);
     free(s->prev);
     free(s->curr);
     free(s->c2dt2);
@@ -466,6 +469,37 @@ void fdwo_solver_destroy(fdwo_solver* s) {
 }
 
 void fdwo_solver_set_threads(fdwo_solver* s, int threads) { s->threads = threads; }
+
+int fdwo_density_log_gradient(const fdwo_grid* g, int dtype, const void* rho, void* grad) {
+    double w[10];
+    if (fdwo_first_derivative_coefficients(g->space_order, w)) return FDWO_EINVAL;
+    const uint64_t n = g->padded[0] * g->padded[1] * g->padded[2];
+    memset(grad, 0, 3 * n * dtype);
+    if (dtype == 4)
+        density_log_gradient_f32(g, w, (const float*)rho, (float*)grad);
+    else
+        density_log_gradient_f64(g, w, (const double*)rho, (double*)grad);
+    return FDWO_OK;
+}
+
+int fdwo_solver_set_density(fdwo_solver* s, const void* rho) {
+    const uint64_t n = s->g.padded[0] * s->g.padded[1] * s->g.padded[2];
+    void* buf = calloc(3 * n, s->dtype);
+    if (!buf) return FDWO_ENOMEM;
+    int rc = fdwo_density_log_gradient(&s->g, s->dtype, rho, buf);
+    if (rc) {
+        free(buf);
+        return rc;
+    }
+    for (int a = 0; a < 3; ++a) {
+        free(s->grad[a]);
+        s->grad[a] = malloc(n * s->dtype);
+        memcpy(s->grad[a], (char*)buf + a * n * s->dtype, n * s->dtype);
+    }
+    free(buf);
+    fdwo_first_derivative_coefficients(s->g.space_order, s->w);
+    return FDWO_OK;
+}
 
 static int copy_csr(uint64_t n, const uint64_t* off, const uint64_t* idx, const double* w,
                     uint64_t** o_off, uint64_t** o_idx, double** o_w) {

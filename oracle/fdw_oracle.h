@@ -88,6 +88,11 @@ int fdwo_solver_create(const fdwo_grid* g, int dtype, const double* coeffs /* v_
                        const void* velocity_padded, const void* eta_padded,
                        fdwo_solver** out);
 void fdwo_solver_destroy(fdwo_solver* s);
+/* VariableDensity = true (kernel.hpp:104-136 density_log_gradient; sweep terms
+ * :365-373 / :407-417): rho is the padded density field of T. */
+int fdwo_solver_set_density(fdwo_solver* s, const void* rho_padded);
+/* density_log_gradient alone: grad[axis] padded fields of T (3 x padded size). */
+int fdwo_density_log_gradient(const fdwo_grid* g, int dtype, const void* rho_padded, void* grad_out);
 void fdwo_solver_set_threads(fdwo_solver* s, int threads); /* 0: all, 1: serial */
 int fdwo_solver_set_sources(fdwo_solver* s, uint64_t n_points, const uint64_t* offsets,
                             const uint64_t* idx, const double* w, const double* wavelet,

@@ -89,6 +89,8 @@ def olib():
         L.fdwo_solver_create.argtypes = [C.POINTER(fdwo_grid), C.c_int, _DP, C.c_double, _U64, _P, _P, _P,
                                          C.POINTER(_P)]
         L.fdwo_solver_destroy.argtypes = [_P]
+        L.fdwo_solver_set_density.argtypes = [_P, _P]
+        L.fdwo_density_log_gradient.argtypes = [C.POINTER(fdwo_grid), C.c_int, _P, _P]
         L.fdwo_solver_set_threads.argtypes = [_P, C.c_int]
         L.fdwo_solver_set_sources.argtypes = [_P, _U64, _P, _P, _P, _P, _U64]
         L.fdwo_solver_set_receivers.argtypes = [_P, _U64, _P, _P, _P]
@@ -122,6 +124,9 @@ def rlib():
         L.ref_solver_create.restype = _P
         L.ref_solver_create.argtypes = [C.c_int, C.c_int, C.c_int, _P, _P, C.c_double, _U64, _P, _P, _P]
         L.ref_destroy.argtypes = [_P]
+        L.ref_solver_create_vd.restype = _P
+        L.ref_solver_create_vd.argtypes = [C.c_int, C.c_int, C.c_int, _P, _P, C.c_double, _U64, _P, _P, _P, _P]
+        L.ref_density_log_gradient.argtypes = [C.c_int, C.c_int, C.c_int, _P, _P, _P, _P]
         L.ref_info.restype = _U64
         L.ref_info.argtypes = [_P, _P, _DP, _U64P, _U64P]
         L.ref_get_fields.argtypes = [_P, _P, _P]
@@ -166,7 +171,8 @@ def oracle_grid(ndim, bbox, spacing, order, damping):
 class OracleSolver:
     """fdwo_solver handle: the C restatement of Solver<T> on caller arrays."""
 
-    def __init__(self, ndim, order, dtype, extended, spacing, dt, n_steps, bc, velocity, eta, threads=0):
+    def __init__(self, ndim, order, dtype, extended, spacing, dt, n_steps, bc, velocity, eta, threads=0,
+                 density=None):
         L = olib()
         g = fdwo_grid()
         g.ndim, g.halo, g.space_order = ndim, order // 2, order
@@ -190,6 +196,10 @@ class OracleSolver:
         L.fdwo_solver_set_threads(self.h, threads)
         self.n_steps = n_steps
         self.n_rec = 0
+        if density is not None:
+            self.rho = np.ascontiguousarray(density, self.dtype).reshape(self.shape)
+            if L.fdwo_solver_set_density(self.h, _ptr(self.rho)):
+                raise ValueError("fdwo_solver_set_density failed")
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -346,7 +356,7 @@ class RefRun:
 class RefSolver:
     """Reference Solver<T> built on caller arrays (test_kernel.cpp make_solver style)."""
 
-    def __init__(self, ndim, order, dtype, extended, spacing, dt, n_steps, bc, velocity, eta):
+    def __init__(self, ndim, order, dtype, extended, spacing, dt, n_steps, bc, velocity, eta, density=None):
         L = rlib()
         if L is None:
             raise RuntimeError("reference library not built")
@@ -357,8 +367,9 @@ class RefSolver:
         self.vel = np.ascontiguousarray(velocity, self.dtype)
         self.eta = np.ascontiguousarray(eta, self.dtype)
         bcs = np.array([[int(bc[a][s]) for s in range(2)] for a in range(3)], np.int32)
-        self.h = L.ref_solver_create(ndim, order, self.dtype.itemsize, _ptr(ext), _ptr(sp), dt, n_steps, _ptr(bcs),
-                                     _ptr(self.vel), _ptr(self.eta))
+        self.rho = None if density is None else np.ascontiguousarray(density, self.dtype)
+        self.h = L.ref_solver_create_vd(ndim, order, self.dtype.itemsize, _ptr(ext), _ptr(sp), dt, n_steps,
+                                        _ptr(bcs), _ptr(self.vel), _ptr(self.eta), _ptr(self.rho))
         if not self.h:
             raise ValueError(L.ref_last_error().decode())
         self.n_steps = n_steps

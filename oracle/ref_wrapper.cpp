@@ -179,7 +179,8 @@ RunBase* make_run(const ref_config* cfg, const double* raw, const uint64_t* raw_
 template <typename T>
 RunBase* make_solver_from_arrays(int ndim, int order, const uint64_t* extended,
                                  const double* spacing, double dt, uint64_t n_steps,
-                                 const int32_t bc[3][2], const void* vel, const void* eta) {
+                                 const int32_t bc[3][2], const void* vel, const void* eta,
+                                 const void* rho = nullptr) {
     auto run = std::make_unique<Run<T>>();
     Grid grid;
     grid.ndim = ndim;
@@ -199,6 +200,11 @@ RunBase* make_solver_from_arrays(int ndim, int order, const uint64_t* extended,
     run->eta_copy = e;
     MaterialModel<T> materials;  // bypass the >0 check so tests may pass any field
     materials.velocity = std::move(v);
+    if (rho) {  // VariableDensity = true branch of the sweep (kernel.hpp:365-373, :407-417)
+        Field<T> r(ndim, padded);
+        std::memcpy(r.data(), rho, r.size() * sizeof(T));
+        materials.density = std::move(r);
+    }
     DampingField<T> damping;
     damping.eta = std::move(e);
     TimeAxis axis;
@@ -247,6 +253,50 @@ void* ref_solver_create(int ndim, int order, int dtype, const uint64_t* extended
         g_err = e.what();
         return nullptr;
     }
+}
+
+void* ref_solver_create_vd(int ndim, int order, int dtype, const uint64_t* extended,
+                           const double* spacing, double dt, uint64_t n_steps, const int32_t* bc,
+                           const void* vel, const void* eta, const void* rho) {
+    try {
+        const auto* b = reinterpret_cast<const int32_t(*)[2]>(bc);
+        if (dtype == 4)
+            return make_solver_from_arrays<float>(ndim, order, extended, spacing, dt, n_steps, b,
+                                                  vel, eta, rho);
+        return make_solver_from_arrays<double>(ndim, order, extended, spacing, dt, n_steps, b, vel,
+                                               eta, rho);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+// density_log_gradient (kernel.hpp:104-136) of a padded rho: 3 padded fields out
+void ref_density_log_gradient(int ndim, int order, int dtype, const uint64_t* extended,
+                              const double* spacing, const void* rho, void* out) {
+    Grid grid;
+    grid.ndim = ndim;
+    grid.space_order = order;
+    grid.halo = order / 2;
+    for (int a = 0; a < ndim; ++a) {
+        grid.extended_shape[a] = extended[a];
+        grid.spacing[a] = spacing[a];
+    }
+    const auto padded = grid.padded_shape();
+    auto run = [&](auto tag) {
+        using T = decltype(tag);
+        Field<T> r(ndim, padded);
+        std::memcpy(r.data(), rho, r.size() * sizeof(T));
+        const auto g = density_log_gradient(r, grid, make_stencil(order));
+        for (int a = 0; a < 3; ++a)
+            if (g[a].size())
+                std::memcpy(static_cast<char*>(out) + a * r.size() * sizeof(T), g[a].data(),
+                            r.size() * sizeof(T));
+    };
+    if (dtype == 4)
+        run(float{});
+    else
+        run(double{});
 }
 
 void ref_destroy(void* h) { delete static_cast<RunBase*>(h); }

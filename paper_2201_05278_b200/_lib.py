@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FDW_LIB") or os.path.join(_HERE, "libfdwave_cuda.so")  # FDW_LIB: A/B builds
 
-FDW_ABI_VERSION = 1
+FDW_ABI_VERSION = 2
 FDW_OK, FDW_EINVAL, FDW_ECUDA, FDW_ENCCL, FDW_EINSTABLE, FDW_ENOMEM, FDW_ESTATE = range(7)
 FDW_KERNEL_AUTO, FDW_KERNEL_SIMPLE, FDW_KERNEL_ZMARCH, FDW_KERNEL_TMA, FDW_KERNEL_FUSED2D = 0, 1, 2, 3, 4
 FDW_MATH_EXACT, FDW_MATH_FMA = 0, 1
@@ -41,6 +41,7 @@ class fdw_desc(C.Structure):
         ("z_begin", C.c_uint64),
         ("z_end", C.c_uint64),
         ("nccl_id", C.c_ubyte * 128),
+        ("coeffs1", C.c_double * 10),
     ]
 
 
@@ -57,6 +58,7 @@ _SIGS = {
     "fdw_status_string": (C.c_char_p, [C.c_int]),
     "fdw_set_stream": (C.c_int, [_P, _P]),
     "fdw_set_medium": (C.c_int, [_P, _P, _P, C.c_int]),
+    "fdw_set_density": (C.c_int, [_P, _P, C.c_int]),
     "fdw_set_sources": (C.c_int, [_P, C.c_uint64, _P, _P, _P, _P, C.c_uint64]),
     "fdw_set_receivers": (C.c_int, [_P, C.c_uint64, _P, _P, _P]),
     "fdw_set_levels": (C.c_int, [_P, _P, _P]),

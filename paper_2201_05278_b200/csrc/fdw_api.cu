@@ -63,6 +63,8 @@ struct fdw_solver {
     int gstate[2] = {0, 0};
     void* c2dt2 = nullptr;
     void* eta = nullptr;
+    void* grad[3] = {nullptr, nullptr, nullptr};  // variable density: grad(rho)/rho per axis
+    bool vd = false;
     Ctrl* ctrl = nullptr;
     Ctrl* h_ctrl = nullptr;  // pinned mirror
     bool medium_set = false;
@@ -256,6 +258,14 @@ SweepArgs<T> sweep_args(fdw_solver* c, int src, int dst) {
         a.gact[0][1] = c->d.rank == c->d.world - 1;
     }
     a.ctrl = c->ctrl;
+    if (c->vd) {
+        a.vd = 1;
+        for (int k = 0; k < 3; ++k) {
+            a.grad[k] = static_cast<const T*>(c->grad[k < c->ndim ? k : 0]);
+            a.i2h[k] = k < c->ndim ? static_cast<T>(1.0 / (2.0 * c->d.spacing[k])) : T(0);
+        }
+        for (int j = 0; j < c->R; ++j) a.w1[j] = static_cast<T>(c->d.coeffs1[j]);
+    }
     return a;
 }
 
@@ -832,6 +842,25 @@ fdw_status run_chunk(fdw_solver* c, unsigned long long L, bool check, bool recor
     return FDW_OK;
 }
 
+template <typename T>
+fdw_status density_grad_t(fdw_solver* c, const T* rho) {
+    // extended points of the local slab; per-axis strides of the device layout
+    const long long nz = c->nzl, nx = c->nxl, ny = c->ndim == 3 ? c->nyl : 1;
+    const long long stride[3] = {c->ndim == 3 ? c->plane : c->ld, c->ndim == 3 ? c->ld : 1, 1};
+    const long long n = nz * nx * ny;
+    double w[10] = {0};
+    for (int j = 0; j < c->R; ++j) w[j] = c->d.coeffs1[j];
+    const int tb = 256;
+    for (int ax = 0; ax < c->ndim; ++ax) {
+        fdw::density_grad_kernel<T><<<(unsigned)((n + tb - 1) / tb), tb, 0, c->stream>>>(
+            rho, static_cast<T*>(c->grad[ax]), c->origin, stride[1], stride[0], (int)nz, (int)nx, (int)ny,
+            stride[ax], c->R, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], w[8], w[9],
+            1.0 / (2.0 * c->d.spacing[ax]));
+        CHECK_LAUNCH();
+    }
+    return FDW_OK;
+}
+
 // Materialises the stored ghost cells of a level whose ghosts are virtual.
 fdw_status settle_ghosts(fdw_solver* c, int lv) {
     if (c->gstate[lv] != 1) return FDW_OK;
@@ -1224,7 +1253,7 @@ fdw_status fdw_destroy(fdw_solver* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     if (c->comm) ncclCommDestroy(c->comm);
-    for (void* p : {c->lvl[0], c->lvl[1], c->c2dt2, c->eta})
+    for (void* p : {c->lvl[0], c->lvl[1], c->c2dt2, c->eta, c->grad[0], c->grad[1], c->grad[2]})
         if (p) cudaFreeAsync(p, c->stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void* p : {(void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off, (void*)c->d_ent_w, (void*)c->d_wavelet,
@@ -1268,6 +1297,39 @@ fdw_status fdw_set_medium(fdw_solver* c, const void* velocity, const void* eta, 
     CHECK_LAUNCH();
     CU(cudaStreamSynchronize(c->stream));
     c->medium_set = true;
+    return FDW_OK;
+}
+
+fdw_status fdw_set_density(fdw_solver* c, const void* rho, int on_device) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (!rho) return fail(c, FDW_EINVAL, "density is required");
+    for (int j = 0; j < c->R; ++j)
+        if (!std::isfinite(c->d.coeffs1[j]) || (j == 0 && c->d.coeffs1[0] == 0.0))
+            return fail(c, FDW_EINVAL, "desc.coeffs1 (first-derivative weights) must be set for variable density");
+    const size_t bytes = c->level_elems * c->tsize;
+    void* tmp = nullptr;
+    CU(cudaMallocAsync(&tmp, bytes, c->stream));
+    CU(cudaMemsetAsync(tmp, 0, bytes, c->stream));
+    for (int ax = 0; ax < c->ndim; ++ax)
+        if (!c->grad[ax]) {
+            CU(cudaMallocAsync(&c->grad[ax], bytes, c->stream));
+            CU(cudaMemsetAsync(c->grad[ax], 0, bytes, c->stream));
+        }
+    if ((s = copy_host_to_level(c, tmp, rho, on_device))) return s;
+    s = c->tsize == 4 ? density_grad_t<float>(c, static_cast<const float*>(tmp))
+                      : density_grad_t<double>(c, static_cast<const double*>(tmp));
+    cudaFreeAsync(tmp, c->stream);
+    if (s) return s;
+    // the density terms live in the stored-ghost element-wise sweep: move any
+    // virtual-ghost level to stored ghosts and switch variant
+    if ((s = settle_ghosts(c, 0))) return s;
+    if ((s = settle_ghosts(c, 1))) return s;
+    c->variant = FDW_KERNEL_SIMPLE;
+    c->vd = true;
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    CU(cudaStreamSynchronize(c->stream));
     return FDW_OK;
 }
 

@@ -94,6 +94,11 @@ struct SweepArgs {
     // +1 Neumann, 0 none) and whether the face is physical on this rank
     int gf[3][2];
     int gact[3][2];
+    // variable density (simple kernels): grad(rho)/rho per axis, w_1..w_r, 1/(2h)
+    const T* grad[3];
+    T w1[10];
+    T i2h[3];
+    int vd;
     const Ctrl* ctrl;
 };
 
@@ -117,7 +122,19 @@ __global__ void __launch_bounds__(256) sweep3d_simple(SweepArgs<T> a) {
         lx = A::add(lx, A::mul(a.v[j], A::add(__ldg(u + i + j * a.ld), __ldg(u + i - j * a.ld))));
         ly = A::add(ly, A::mul(a.v[j], A::add(__ldg(u + i + j), __ldg(u + i - j))));
     }
-    const T rhs = A::add(A::add(A::mul(lz, a.ih[0]), A::mul(lx, a.ih[1])), A::mul(ly, a.ih[2]));
+    T rhs = A::add(A::add(A::mul(lz, a.ih[0]), A::mul(lx, a.ih[1])), A::mul(ly, a.ih[2]));
+    if (a.vd) {  // kernel.hpp:407-417
+        T dz = T(0), dx = T(0), dy = T(0);
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+            dz = A::add(dz, A::mul(a.w1[j - 1], A::sub(__ldg(u + i + j * a.plane), __ldg(u + i - j * a.plane))));
+            dx = A::add(dx, A::mul(a.w1[j - 1], A::sub(__ldg(u + i + j * a.ld), __ldg(u + i - j * a.ld))));
+            dy = A::add(dy, A::mul(a.w1[j - 1], A::sub(__ldg(u + i + j), __ldg(u + i - j))));
+        }
+        rhs = A::sub(rhs, A::add(A::add(A::mul(A::mul(__ldg(a.grad[0] + i), dz), a.i2h[0]),
+                                        A::mul(A::mul(__ldg(a.grad[1] + i), dx), a.i2h[1])),
+                                 A::mul(A::mul(__ldg(a.grad[2] + i), dy), a.i2h[2])));
+    }
     a.out[i] = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
 }
 
@@ -138,7 +155,17 @@ __global__ void __launch_bounds__(256) sweep2d_simple(SweepArgs<T> a) {
         lz = A::add(lz, A::mul(a.v[j], A::add(__ldg(u + i + j * a.ld), __ldg(u + i - j * a.ld))));
         lx = A::add(lx, A::mul(a.v[j], A::add(__ldg(u + i + j), __ldg(u + i - j))));
     }
-    const T rhs = A::add(A::mul(lz, a.ih[0]), A::mul(lx, a.ih[1]));
+    T rhs = A::add(A::mul(lz, a.ih[0]), A::mul(lx, a.ih[1]));
+    if (a.vd) {  // kernel.hpp:365-373
+        T dz = T(0), dx = T(0);
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+            dz = A::add(dz, A::mul(a.w1[j - 1], A::sub(__ldg(u + i + j * a.ld), __ldg(u + i - j * a.ld))));
+            dx = A::add(dx, A::mul(a.w1[j - 1], A::sub(__ldg(u + i + j), __ldg(u + i - j))));
+        }
+        rhs = A::sub(rhs, A::add(A::mul(A::mul(__ldg(a.grad[0] + i), dz), a.i2h[0]),
+                                 A::mul(A::mul(__ldg(a.grad[1] + i), dx), a.i2h[1])));
+    }
     a.out[i] = time_update<T, EXACT>(rhs, uc, __ldg(a.c2dt2 + i), a.out[i], __ldg(a.eta + i), a.dt);
 }
 
@@ -822,6 +849,28 @@ __global__ void __launch_bounds__(256) boundary_kernel(T* f, BoundaryArgs b, con
         const T v = f[src];
         *dst = fac < 0 ? -v : v;
     }
+}
+
+// density_log_gradient, kernel.hpp:104-136, one axis: over extended points
+// g = T(acc * inv2h / double(rho)), acc = sum_j w_j (double(rho+) - double(rho-)).
+template <typename T>
+__global__ void density_grad_kernel(const T* __restrict__ rho, T* __restrict__ g, long long origin, long long ld,
+                                    long long plane, int nz, int nx, int ny, long long stride, int R, double w0,
+                                    double w1, double w2, double w3, double w4, double w5, double w6, double w7,
+                                    double w8, double w9, double inv2h) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long n = (long long)nz * nx * ny;
+    if (t >= n) return;
+    const int y = (int)(t % ny);
+    const long long r2 = t / ny;
+    const int x = (int)(r2 % nx), z = (int)(r2 / nx);
+    const long long i = origin + (long long)z * plane + (long long)x * ld + y;
+    const double w[10] = {w0, w1, w2, w3, w4, w5, w6, w7, w8, w9};
+    double acc = 0.0;
+    for (int j = 1; j <= R; ++j)
+        acc = __dadd_rn(acc, __dmul_rn(w[j - 1], __dsub_rn(static_cast<double>(rho[i + j * stride]),
+                                                           static_cast<double>(rho[i - j * stride]))));
+    g[i] = static_cast<T>(__ddiv_rn(__dmul_rn(acc, inv2h), static_cast<double>(rho[i])));
 }
 
 // ---------------------------------------------------------------------------

@@ -137,8 +137,6 @@ class Solver:
                  slab=None):
         if coeffs.order != grid.space_order:
             raise ValueError("stencil order does not match grid order")
-        if materials.density is not None:
-            raise ValueError("variable density is not supported on the CUDA path")
         L = _lib.lib()
         self._grid = grid
         self._time = time_axis
@@ -161,6 +159,8 @@ class Solver:
                 d.bc[a][s] = int(boundary.face[a][s])
         for j, v in enumerate(coeffs.second):
             d.coeffs[j] = float(v)
+        for j, v in enumerate(coeffs.first):
+            d.coeffs1[j] = float(v)
         d.dt = float(time_axis.dt)
         d.n_steps = int(time_axis.n_steps)
         d.device = int(device)
@@ -186,6 +186,11 @@ class Solver:
             raise FdwError(f"fdw_create: {msg} (status {rc})")
         self._desc = d
         _check(self._ctx, L.fdw_set_medium(self._ctx, ptr(vel), ptr(eta), 0), "fdw_set_medium")
+        if materials.density is not None:  # kernel.hpp:295-296
+            rho = np.ascontiguousarray(materials.density, dtype=self._dtype)
+            if rho.size != vel.size:
+                raise ValueError("density shape does not match the padded grid")
+            _check(self._ctx, L.fdw_set_density(self._ctx, ptr(rho), 0), "fdw_set_density")
         self._sources = None
         self._wavelet = None
         self._receivers = None

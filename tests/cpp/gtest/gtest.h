@@ -101,9 +101,13 @@ inline void InitGoogleTest(int*, char**) {}
         #suite, #name, &GTS_CAT(gts_body_, GTS_CAT(suite, GTS_CAT(_, name))));                     \
     static void GTS_CAT(gts_body_, GTS_CAT(suite, GTS_CAT(_, name)))()
 
+// switch(0) case 0: default: keeps a caller's trailing `else` unambiguous (as GTest does)
 #define GTS_CMP(fatal, op, a, b)                                                                   \
-    if (const auto& gts_a = (a); true)                                                              \
-        if (const auto& gts_b = (b); gts_a op gts_b) {                                              \
+    switch (0)                                                                                     \
+    case 0:                                                                                        \
+    default:                                                                                       \
+        if (const auto& gts_a = (a); false) {                                                      \
+        } else if (const auto& gts_b = (b); gts_a op gts_b) {                                      \
         } else                                                                                     \
             ::testing::Reporter(fatal, __FILE__, __LINE__,                                          \
                                 ::testing::describe(#op, #a, #b, gts_a, gts_b))
@@ -124,6 +128,9 @@ inline void InitGoogleTest(int*, char**) {}
 #define ASSERT_DOUBLE_EQ(a, b) ASSERT_EQ(a, b)
 
 #define GTS_NEAR(fatal, a, b, tol)                                                                 \
+    switch (0)                                                                                     \
+    case 0:                                                                                        \
+    default:                                                                                       \
     if (const double gts_d = std::abs(static_cast<double>(a) - static_cast<double>(b));            \
         gts_d <= static_cast<double>(tol)) {                                                       \
     } else                                                                                         \
@@ -135,6 +142,9 @@ inline void InitGoogleTest(int*, char**) {}
 #define ASSERT_NEAR(a, b, tol) GTS_NEAR(true, a, b, tol)
 
 #define GTS_BOOL(fatal, c, want)                                                                   \
+    switch (0)                                                                                     \
+    case 0:                                                                                        \
+    default:                                                                                       \
     if (static_cast<bool>(c) == want) {                                                            \
     } else                                                                                         \
         ::testing::Reporter(fatal, __FILE__, __LINE__, std::string("Value of: ") + #c)
@@ -144,6 +154,9 @@ inline void InitGoogleTest(int*, char**) {}
 #define ASSERT_FALSE(c) GTS_BOOL(true, c, false)
 
 #define GTS_THROW(fatal, stmt, exc)                                                                \
+    switch (0)                                                                                     \
+    case 0:                                                                                        \
+    default:                                                                                       \
     if (bool gts_ok = [&] {                                                                        \
             try {                                                                                  \
                 stmt;                                                                              \
@@ -162,6 +175,9 @@ inline void InitGoogleTest(int*, char**) {}
 #define EXPECT_ANY_THROW(stmt) GTS_THROW(false, stmt, std::exception)
 
 #define GTS_NOTHROW(fatal, stmt)                                                                   \
+    switch (0)                                                                                     \
+    case 0:                                                                                        \
+    default:                                                                                       \
     if (bool gts_ok = [&] {                                                                        \
             try {                                                                                  \
                 stmt;                                                                              \

@@ -43,7 +43,7 @@ def test_desc_layout_matches_c():
     _lib.lib().fdw_desc_init(C.byref(d))
     assert d.abi_version == _lib.FDW_ABI_VERSION
     assert d.check_interval == 100 and d.world == 1 and d.dtype_bytes == 4
-    assert C.sizeof(_lib.fdw_desc) == 368
+    assert C.sizeof(_lib.fdw_desc) == 448
 
 
 @pytest.mark.parametrize("n,world", [(217, 1), (217, 2), (217, 8), (1600, 8), (19, 3)])

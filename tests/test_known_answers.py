@@ -22,7 +22,8 @@ class OracleAPI:
 
     def __init__(self, grid, materials, damping, spec, axis, coeffs):
         self._s = O.OracleSolver(grid.ndim, grid.space_order, np.float64, grid.extended_shape, grid.spacing,
-                                 axis.dt, axis.n_steps, spec.face, materials.velocity, damping.eta)
+                                 axis.dt, axis.n_steps, spec.face, materials.velocity, damping.eta,
+                                 density=materials.density)
         self._axis = axis
         self._grid = grid
         self._n_rec = 0
@@ -79,12 +80,12 @@ def backend(request):
 
 
 def make_solver(backend, extent_z=8.0, extent_x=8.0, h=1.0, c=1.0, order=2, dt=0.1, steps=1,
-                damping_length=0.0, alpha=0.0, power=3.0, bc=BC.None_, stride=0):
+                damping_length=0.0, alpha=0.0, power=3.0, bc=BC.None_, stride=0, rho=None):
     """test_kernel.cpp:37-66 make_solver."""
     grid = build_grid([0, extent_z, 0, extent_x], [h, h], order, Precision.Double)
     grid = extend_with_damping(grid, [damping_length] * 4)
     vel = np.full(grid.padded_shape()[:2], c, np.float64)
-    mats = make_material_model(vel)
+    mats = make_material_model(vel, None if rho is None else np.full_like(vel, rho))
     damp = damping_field(grid, alpha, power, np.float64)
     axis = TimeAxis(tf=dt * steps, dt=dt, n_steps=steps, saving_stride=stride,
                     stable_bound=stable_dt(c, [h, h], order, 2))
@@ -312,11 +313,15 @@ def test_snapshot_memory_guard():  # :506-520
         s.forward()
 
 
-@pytest.mark.gpu
-def test_variable_density_is_rejected_on_the_cuda_path():  # :102-123 needs VariableDensity=true
-    grid = extend_with_damping(build_grid([0, 40, 0, 40], [1, 1], 2, Precision.Double), [0] * 4)
-    vel = np.ones(grid.padded_shape()[:2])
-    mats = make_material_model(vel, np.full_like(vel, 2.7))
-    with pytest.raises(ValueError):
-        Solver(grid, mats, damping_field(grid, 0, 0, np.float64), BoundarySpec.uniform(BC.NullDirichlet),
-               TimeAxis(tf=6, dt=0.2, n_steps=30), make_stencil(2))
+def test_constant_density_equals_variable_density_with_constant_rho(backend):  # :102-123
+    runs = []
+    for rho in (None, 2.7):
+        s = make_solver(backend, extent_z=40, extent_x=40, dt=0.2, steps=30, bc=BC.NullDirichlet, rho=rho)
+        cur = s.current_level()
+        iz, ix = np.meshgrid(np.arange(cur.shape[0]), np.arange(cur.shape[1]), indexing="ij")
+        cur[...] = np.exp(-((iz - 20.0) ** 2 + (ix - 20.0) ** 2) / 18.0)
+        s.refresh_boundary()
+        for _ in range(30):
+            s.step()
+        runs.append(np.array(s.current_level()))
+    assert np.array_equal(runs[0], runs[1])  # grad(rho) is exactly zero

@@ -79,3 +79,43 @@ def test_first_non_finite_is_reported_like_the_reference():
         s.current()[5, 7] = np.inf
         s.current()[3, 9] = np.nan
     assert np.isnan(r.max_abs()) and np.isnan(o.max_abs())
+
+
+@pytest.mark.parametrize("ndim", [2, 3])
+@pytest.mark.parametrize("order", [2, 4, 8])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_variable_density_branch(ndim, order, dtype):
+    """VariableDensity = true: density_log_gradient + the extra sweep terms
+    (kernel.hpp:104-136, :365-373, :407-417), bit-identical."""
+    ext = (14, 16) if ndim == 2 else (12, 13, 14)
+    ext = tuple(e + order for e in ext)
+    rng = np.random.default_rng(11 + order)
+    pad = tuple(e + order for e in ext)
+    vel = (1500 + 3000 * rng.random(pad)).astype(dtype)
+    eta = (20.0 * rng.random(pad)).astype(dtype)
+    rho = (1.0 + 2.0 * rng.random(pad)).astype(dtype)
+    sp = [10.0, 12.0, 9.0][:ndim]
+    args = (ndim, order, dtype, ext, sp, 0.3 * 9.0 / 4500.0, 250, [[N, D], [X, D], [D, N]], vel, eta)
+    r, o = O.RefSolver(*args, density=rho), O.OracleSolver(*args, density=rho)
+    g_ref = np.zeros((3,) + pad, dtype)
+    REF.ref_density_log_gradient(ndim, order, np.dtype(dtype).itemsize,
+                                 np.array(list(ext) + [1] * (3 - ndim), np.uint64).ctypes.data_as(C.c_void_p),
+                                 np.array(sp + [1.0] * (3 - ndim)).ctypes.data_as(C.c_void_p),
+                                 rho.ctypes.data_as(C.c_void_p), g_ref.ctypes.data_as(C.c_void_p))
+    g_or = np.zeros((3,) + pad, dtype)
+    grid = O.fdwo_grid()
+    grid.ndim, grid.halo, grid.space_order = ndim, order // 2, order
+    for a in range(3):
+        grid.spacing[a] = sp[a] if a < ndim else 1.0
+        grid.extended[a] = ext[a] if a < ndim else 1
+        grid.padded[a] = pad[a] if a < ndim else 1
+    O.olib().fdwo_density_log_gradient(C.byref(grid), np.dtype(dtype).itemsize, rho.ctypes.data_as(C.c_void_p),
+                                       g_or.ctypes.data_as(C.c_void_p))
+    assert same(g_ref[:ndim], g_or[:ndim])
+    a = rng.standard_normal(r.shape).astype(dtype)
+    for s_ in (r, o):
+        s_.current()[...] = a
+        s_.refresh_boundary()
+    for _ in range(5):
+        assert r.step() == o.step()
+        assert same(r.current(), o.current())
