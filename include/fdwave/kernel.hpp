@@ -20,8 +20,8 @@
 //
 // Variable density (MaterialModel::density) runs on the GPU through
 // fdw_set_density (grad(rho)/rho formed on the device, kernel.hpp:104-136 and
-// :295-296).  Not on the CUDA path (throws std::invalid_argument, as SURVEY.md
-// 8b specifies): add_volume_source.  set_backend is accepted and ignored.
+// :295-296); add_volume_source through fdw_add_volume_source (:199-203,
+// :439-452).  set_backend is accepted and ignored.
 #pragma once
 
 #include <array>
@@ -268,7 +268,11 @@ public:
     void add_volume_source(ModulatedField<T> source) {
         if (source.amplitude.size() < time_.n_steps)
             throw std::invalid_argument("volume source amplitude shorter than run");
-        throw std::invalid_argument("volume sources are not supported on the CUDA path");
+        const auto pad = grid_.padded_shape();
+        if (source.field.size() != pad[0] * pad[1] * pad[2])
+            throw std::invalid_argument("volume source field shape mismatch");
+        check(fdw_add_volume_source(ctx_, source.field.data(), source.amplitude.data(), source.amplitude.size(), 0),
+              "fdw_add_volume_source");
     }
     void set_backend(Backend, int) {}
     void set_verbose(bool verbose) { verbose_ = verbose; }

@@ -122,6 +122,13 @@ fdw_status fdw_set_medium(fdw_solver* ctx, const void* velocity, const void* eta
  * desc.coeffs1.  Padded slab of T (host, or device with on_device = 1). */
 fdw_status fdw_set_density(fdw_solver* ctx, const void* rho, int on_device);
 
+/* Solver<T>::add_volume_source, kernel.hpp:199-203 (ModulatedField, :140-144;
+ * applied in inject, :439-452): a padded forcing field of T (host, or device
+ * with on_device = 1) and one double amplitude per step (n_amp >= n_steps,
+ * else FDW_EINVAL).  Sources accumulate in call order. */
+fdw_status fdw_add_volume_source(fdw_solver* ctx, const void* field, const double* amplitude, uint64_t n_amp,
+                                 int on_device);
+
 /* Solver<T>::set_sources, kernel.hpp:188-193: CSR view of an InterpolationMap
  * (offsets[n_points+1], idx/w[offsets[n_points]]) plus the wavelet (double,
  * >= n_steps + 1 samples when n_points > 0).  Entries outside this rank's slab

@@ -398,6 +398,11 @@ struct fdwo_solver {
     uint64_t *src_off, *src_idx, *rec_off, *rec_idx;
     double *src_w, *rec_w, *wavelet;
     uint64_t n_wavelet;
+    /* volume sources (ModulatedField, kernel.hpp:140-144), insertion order */
+    uint64_t n_vol;
+    void** vol_field;    /* padded fields of T */
+    double** vol_amp;    /* per-step amplitudes */
+    uint64_t* vol_namp;
 };
 
 #define T float
@@ -465,6 +470,13 @@ void fdwo_solver_destroy(fdwo_solver* s) {
     free(s->rec_idx);
     free(s->rec_w);
     free(s->wavelet);
+    for (uint64_t q = 0; q < s->n_vol; ++q) {
+        free(s->vol_field[q]);
+        free(s->vol_amp[q]);
+    }
+    free(s->vol_field);
+    free(s->vol_amp);
+    free(s->vol_namp);
     free(s);
 }
 
@@ -498,6 +510,30 @@ int fdwo_solver_set_density(fdwo_solver* s, const void* rho) {
     }
     free(buf);
     fdwo_first_derivative_coefficients(s->g.space_order, s->w);
+    return FDWO_OK;
+}
+
+/* kernel.hpp:199-203 add_volume_source */
+int fdwo_solver_add_volume_source(fdwo_solver* s, const void* field, const double* amp, uint64_t n_amp) {
+    if (n_amp < s->n_steps) return FDWO_EINVAL;
+    const uint64_t n = s->g.padded[0] * s->g.padded[1] * s->g.padded[2];
+    const uint64_t q = s->n_vol;
+    void** vf = (void**)realloc(s->vol_field, (q + 1) * sizeof(void*));
+    if (!vf) return FDWO_ENOMEM;
+    s->vol_field = vf;
+    double** va = (double**)realloc(s->vol_amp, (q + 1) * sizeof(double*));
+    if (!va) return FDWO_ENOMEM;
+    s->vol_amp = va;
+    uint64_t* vn = (uint64_t*)realloc(s->vol_namp, (q + 1) * sizeof(uint64_t));
+    if (!vn) return FDWO_ENOMEM;
+    s->vol_namp = vn;
+    s->vol_field[q] = malloc(n * s->dtype);
+    s->vol_amp[q] = (double*)malloc((n_amp ? n_amp : 1) * sizeof(double));
+    if (!s->vol_field[q] || !s->vol_amp[q]) return FDWO_ENOMEM;
+    memcpy(s->vol_field[q], field, n * s->dtype);
+    if (n_amp) memcpy(s->vol_amp[q], amp, n_amp * sizeof(double));
+    s->vol_namp[q] = n_amp;
+    s->n_vol = q + 1;
     return FDWO_OK;
 }
 

@@ -93,6 +93,10 @@ void fdwo_solver_destroy(fdwo_solver* s);
 int fdwo_solver_set_density(fdwo_solver* s, const void* rho_padded);
 /* density_log_gradient alone: grad[axis] padded fields of T (3 x padded size). */
 int fdwo_density_log_gradient(const fdwo_grid* g, int dtype, const void* rho_padded, void* grad_out);
+/* kernel.hpp:199-203 add_volume_source: padded field of T, amplitude per step
+ * (n_amp >= n_steps), applied after the point sources (:439-452). */
+int fdwo_solver_add_volume_source(fdwo_solver* s, const void* field_padded, const double* amplitude,
+                                  uint64_t n_amp);
 void fdwo_solver_set_threads(fdwo_solver* s, int threads); /* 0: all, 1: serial */
 int fdwo_solver_set_sources(fdwo_solver* s, uint64_t n_points, const uint64_t* offsets,
                             const uint64_t* idx, const double* w, const double* wavelet,

@@ -92,6 +92,7 @@ def olib():
         L.fdwo_solver_set_density.argtypes = [_P, _P]
         L.fdwo_density_log_gradient.argtypes = [C.POINTER(fdwo_grid), C.c_int, _P, _P]
         L.fdwo_solver_set_threads.argtypes = [_P, C.c_int]
+        L.fdwo_solver_add_volume_source.argtypes = [_P, _P, _P, _U64]
         L.fdwo_solver_set_sources.argtypes = [_P, _U64, _P, _P, _P, _P, _U64]
         L.fdwo_solver_set_receivers.argtypes = [_P, _U64, _P, _P, _P]
         L.fdwo_solver_current.restype = _P
@@ -133,6 +134,7 @@ def rlib():
         L.ref_get_map.argtypes = [_P, C.c_int, _P, _P, _P]
         L.ref_get_wavelet.argtypes = [_P, _P]
         L.ref_set_threads.argtypes = [_P, C.c_int]
+        L.ref_solver_add_volume_source.argtypes = [_P, _P, _P, _U64]
         L.ref_step.argtypes = [_P, _U64P, _DP]
         L.ref_level.restype = _P
         L.ref_level.argtypes = [_P, C.c_int]
@@ -230,6 +232,14 @@ class OracleSolver:
                      np.ascontiguousarray(imap.weight, np.float64))
         olib().fdwo_solver_set_receivers(self.h, imap.n_points, *(_ptr(a) for a in self._rec))
         self.n_rec = imap.n_points
+
+    def add_volume_source(self, field, amplitude):
+        """kernel.hpp:199-203 (ModulatedField, :140-144)."""
+        f = np.ascontiguousarray(field, self.dtype).reshape(self.shape)
+        a = np.ascontiguousarray(amplitude, np.float64)
+        if olib().fdwo_solver_add_volume_source(self.h, _ptr(f), _ptr(a), len(a)):
+            raise ValueError("volume source amplitude shorter than run")
+        self._vol = getattr(self, "_vol", []) + [(f, a)]
 
     def refresh_boundary(self):
         olib().fdwo_solver_refresh_boundary(self.h)
@@ -400,6 +410,12 @@ class RefSolver:
         self._rec = (np.ascontiguousarray(imap.offsets, np.uint64), np.ascontiguousarray(imap.index, np.uint64),
                      np.ascontiguousarray(imap.weight, np.float64))
         rlib().ref_solver_set_receivers(self.h, imap.n_points, *(_ptr(a) for a in self._rec))
+
+    def add_volume_source(self, field, amplitude):
+        f = np.ascontiguousarray(field, self.dtype)
+        a = np.ascontiguousarray(amplitude, np.float64)
+        if rlib().ref_solver_add_volume_source(self.h, _ptr(f), _ptr(a), len(a)):
+            raise ValueError(rlib().ref_last_error().decode())
 
     def refresh_boundary(self):
         rlib().ref_refresh(self.h)

@@ -59,6 +59,8 @@ BoundarySpec to_spec(const int32_t bc[3][2]) {
     return s;
 }
 
+thread_local std::string g_err;
+
 struct RunBase {
     virtual ~RunBase() = default;
     Grid grid;
@@ -75,6 +77,7 @@ struct RunBase {
                         double* bad_max) = 0;
     virtual void set_threads(int threads) = 0;
     virtual void set_maps() = 0;
+    virtual int add_volume(const void* field, const double* amp, uint64_t n_amp) = 0;
 };
 
 template <typename T>
@@ -100,6 +103,19 @@ struct Run : RunBase {
         return which == 0 ? solver->previous_level().data() : solver->current_level().data();
     }
     void refresh() override { solver->refresh_boundary(); }
+    int add_volume(const void* field, const double* amp, uint64_t n_amp) override {
+        fdwave::ModulatedField<T> m;
+        m.field = Field<T>(grid.ndim, grid.padded_shape());
+        std::memcpy(m.field.data(), field, m.field.size() * sizeof(T));
+        m.amplitude.assign(amp, amp + n_amp);
+        try {
+            solver->add_volume_source(std::move(m));
+        } catch (const std::exception& e) {
+            g_err = e.what();
+            return 1;
+        }
+        return 0;
+    }
     double max_abs() override { return solver->max_abs(); }
     void sample(void* row) override {
         const auto r = sample_receivers(solver->current_level(), rec);
@@ -218,7 +234,6 @@ RunBase* make_solver_from_arrays(int ndim, int order, const uint64_t* extended,
     return run.release();
 }
 
-thread_local std::string g_err;
 
 }  // namespace
 
@@ -391,6 +406,11 @@ int ref_solver_set_sources(void* h, uint64_t n, const uint64_t* off, const uint6
         return 1;
     }
     return 0;
+}
+
+// Solver::add_volume_source (kernel.hpp:199-203)
+int ref_solver_add_volume_source(void* h, const void* field, const double* amp, uint64_t n_amp) {
+    return static_cast<RunBase*>(h)->add_volume(field, amp, n_amp);
 }
 
 int ref_solver_set_receivers(void* h, uint64_t n, const uint64_t* off, const uint64_t* idx,

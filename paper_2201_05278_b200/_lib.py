@@ -59,6 +59,7 @@ _SIGS = {
     "fdw_set_stream": (C.c_int, [_P, _P]),
     "fdw_set_medium": (C.c_int, [_P, _P, _P, C.c_int]),
     "fdw_set_density": (C.c_int, [_P, _P, C.c_int]),
+    "fdw_add_volume_source": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_int]),
     "fdw_set_sources": (C.c_int, [_P, C.c_uint64, _P, _P, _P, _P, C.c_uint64]),
     "fdw_set_receivers": (C.c_int, [_P, C.c_uint64, _P, _P, _P]),
     "fdw_set_levels": (C.c_int, [_P, _P, _P]),

@@ -65,6 +65,13 @@ struct fdw_solver {
     void* eta = nullptr;
     void* grad[3] = {nullptr, nullptr, nullptr};  // variable density: grad(rho)/rho per axis
     bool vd = false;
+    // volume sources (ModulatedField): device fields, pointer table, amplitudes
+    std::vector<void*> vs_fields;
+    void* d_vs_ptrs = nullptr;
+    void* d_vs_amp = nullptr;
+    unsigned long long* d_vs_len = nullptr;
+    unsigned long long vs_namp = 0;
+    std::vector<std::vector<double>> vs_amps;  // host copy of the amplitudes
     Ctrl* ctrl = nullptr;
     Ctrl* h_ctrl = nullptr;  // pinned mirror
     bool medium_set = false;
@@ -558,8 +565,33 @@ fdw_status launch_inject_t(fdw_solver* c, int dst, int k) {
     return FDW_OK;
 }
 
+template <typename T>
+fdw_status launch_volume_t(fdw_solver* c, int dst, int k) {
+    if (c->vs_fields.empty()) return FDW_OK;
+    const long long ny = c->ndim == 3 ? c->nyl : 1;
+    const long long n = c->nzl * c->nxl * ny;
+    const int tb = 256;
+    int dface = 0;
+    for (int a = 0; a < c->ndim; ++a)
+        for (int sd = 0; sd < 2; ++sd) {
+            if (c->d.bc[a][sd] != FDW_BC_NULL_DIRICHLET) continue;
+            if (a == 0 && c->ndim == 3 && ((sd == 0 && c->d.rank != 0) || (sd == 1 && c->d.rank != c->d.world - 1)))
+                continue;  // internal slab face
+            dface |= 1 << (2 * a + sd);
+        }
+    fdw::volume_source_kernel<T><<<(unsigned)((n + tb - 1) / tb), tb, 0, c->stream>>>(
+        static_cast<T*>(c->lvl[dst]), static_cast<const T*>(c->c2dt2), static_cast<const T*>(c->eta), c->d.dt,
+        static_cast<const T* const*>(c->d_vs_ptrs), static_cast<const T*>(c->d_vs_amp), c->d_vs_len, (int)c->vs_fields.size(),
+        c->vs_namp, c->origin, c->ndim == 3 ? c->plane : c->ld, c->ndim == 3 ? c->ld : 1, (int)c->nzl,
+        (int)c->nxl, (int)ny, dface, k, c->ctrl);
+    CHECK_LAUNCH();
+    return FDW_OK;
+}
+
 fdw_status launch_inject(fdw_solver* c, int dst, int k) {
-    return c->tsize == 4 ? launch_inject_t<float>(c, dst, k) : launch_inject_t<double>(c, dst, k);
+    fdw_status s = c->tsize == 4 ? launch_inject_t<float>(c, dst, k) : launch_inject_t<double>(c, dst, k);
+    if (s) return s;
+    return c->tsize == 4 ? launch_volume_t<float>(c, dst, k) : launch_volume_t<double>(c, dst, k);
 }
 
 // apply_boundary (kernel.hpp:67-102) on level `lv`: axis 0, 1, 2 in order.
@@ -1255,6 +1287,9 @@ fdw_status fdw_destroy(fdw_solver* c) {
     if (c->comm) ncclCommDestroy(c->comm);
     for (void* p : {c->lvl[0], c->lvl[1], c->c2dt2, c->eta, c->grad[0], c->grad[1], c->grad[2]})
         if (p) cudaFreeAsync(p, c->stream);
+    for (void* p : c->vs_fields) cudaFreeAsync(p, c->stream);
+    for (void* p : {c->d_vs_ptrs, c->d_vs_amp, (void*)c->d_vs_len})
+        if (p) cudaFreeAsync(p, c->stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void* p : {(void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off, (void*)c->d_ent_w, (void*)c->d_wavelet,
                     (void*)c->d_rec_idx, (void*)c->d_rec_off, (void*)c->d_rec_w, (void*)c->d_seis, (void*)c->d_tmap})
@@ -1327,6 +1362,63 @@ fdw_status fdw_set_density(fdw_solver* c, const void* rho, int on_device) {
     if ((s = settle_ghosts(c, 1))) return s;
     c->variant = FDW_KERNEL_SIMPLE;
     c->vd = true;
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status fdw_add_volume_source(fdw_solver* c, const void* field, const double* amplitude, uint64_t n_amp,
+                                 int on_device) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (!field || (!amplitude && n_amp)) return fail(c, FDW_EINVAL, "volume source field and amplitude required");
+    if (n_amp < c->d.n_steps) return fail(c, FDW_EINVAL, "volume source amplitude shorter than run");
+    const size_t bytes = c->level_elems * c->tsize;
+    void* f = nullptr;
+    CU(cudaMallocAsync(&f, bytes, c->stream));
+    CU(cudaMemsetAsync(f, 0, bytes, c->stream));
+    if ((s = copy_host_to_level(c, f, field, on_device))) {
+        cudaFreeAsync(f, c->stream);
+        return s;
+    }
+    // amplitude table [source][step] of T (the reference casts per step,
+    // kernel.hpp:442), rows padded to the longest; per-source lengths gate the add
+    auto& amps = c->vs_amps;
+    amps.emplace_back(amplitude, amplitude + n_amp);
+    c->vs_fields.push_back(f);
+    unsigned long long L = 0;
+    std::vector<unsigned long long> lens;
+    for (auto& a : amps) {
+        L = std::max<unsigned long long>(L, a.size());
+        lens.push_back(a.size());
+    }
+    std::vector<unsigned char> tab(amps.size() * L * c->tsize, 0);
+    for (size_t q = 0; q < amps.size(); ++q)
+        for (unsigned long long j = 0; j < amps[q].size(); ++j) {
+            if (c->tsize == 4)
+                reinterpret_cast<float*>(tab.data())[q * L + j] = static_cast<float>(amps[q][j]);
+            else
+                reinterpret_cast<double*>(tab.data())[q * L + j] = amps[q][j];
+        }
+    CU(cudaStreamSynchronize(c->stream));  // the old tables may still be read by queued work
+    for (void* p : {c->d_vs_amp, c->d_vs_ptrs, (void*)c->d_vs_len})
+        if (p) cudaFreeAsync(p, c->stream);
+    CU(cudaMallocAsync(&c->d_vs_amp, tab.size() ? tab.size() : 1, c->stream));
+    if (tab.size()) CU(cudaMemcpyAsync(c->d_vs_amp, tab.data(), tab.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMallocAsync(&c->d_vs_ptrs, c->vs_fields.size() * sizeof(void*), c->stream));
+    CU(cudaMemcpyAsync(c->d_vs_ptrs, c->vs_fields.data(), c->vs_fields.size() * sizeof(void*),
+                       cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMallocAsync(&c->d_vs_len, lens.size() * sizeof(unsigned long long), c->stream));
+    CU(cudaMemcpyAsync(c->d_vs_len, lens.data(), lens.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                       c->stream));
+    c->vs_namp = L;
+    // the cooperative 2D kernel fuses only point sources
+    if (c->variant == FDW_KERNEL_FUSED2D) {
+        if ((s = settle_ghosts(c, 0))) return s;
+        if ((s = settle_ghosts(c, 1))) return s;
+        c->variant = FDW_KERNEL_SIMPLE;
+    }
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
     CU(cudaStreamSynchronize(c->stream));

@@ -900,6 +900,42 @@ __global__ void inject_kernel(T* out, const T* __restrict__ c2dt2, const T* __re
     out[i] = val;
 }
 
+// Dense modulated sources, kernel.hpp:439-452: after the point sources, for
+// each source in insertion order, out[i] += c2dt2[i]*field[i]*T(amp[n])*iop[i]
+// over every extended point.  One thread per point, sources looped in order.
+template <typename T>
+__global__ void volume_source_kernel(T* out, const T* __restrict__ c2dt2, const T* __restrict__ eta, double dt,
+                                     const T* const* __restrict__ fields, const T* __restrict__ amps,
+                                     const unsigned long long* __restrict__ amp_len, int n_src,
+                                     unsigned long long n_amp, long long origin, long long plane, long long ld,
+                                     int nz, int nx, int ny, int dface, int k, const Ctrl* ctrl) {
+    using A = Ar<T, true>;
+    if (ctrl->abort) return;
+    const unsigned long long n = ctrl->step + (unsigned long long)k;
+    if (n >= n_amp) return;  // n_amp: the longest amplitude vector
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)nz * nx * ny) return;
+    const int y = (int)(t % ny);
+    const long long r2 = t / ny;
+    const int x = (int)(r2 % nx), z = (int)(r2 / nx);
+    // null-Dirichlet face points are zeroed by apply_boundary right after
+    // (kernel.hpp:87-88): skipping them is exact, and the virtual-ghost
+    // kernels rely on the stored face staying zero
+    if (((dface & 1) && z == 0) || ((dface & 2) && z == nz - 1) || ((dface & 4) && x == 0) ||
+        ((dface & 8) && x == nx - 1) || ((dface & 16) && y == 0) || ((dface & 32) && y == ny - 1))
+        return;
+    const long long i = origin + (long long)z * plane + (long long)x * ld + y;
+    const T c2 = c2dt2[i];
+    const T e = eta[i];
+    T om, iop = T(1);
+    if (e != T(0)) damping_factors(e, dt, om, iop);
+    T val = out[i];
+    for (int q = 0; q < n_src; ++q)
+        if (n < amp_len[q])
+            val = A::add(val, A::mul(A::mul(A::mul(c2, fields[q][i]), amps[(unsigned long long)q * n_amp + n]), iop));
+    out[i] = val;
+}
+
 // apply_boundary, kernel.hpp:67-102, one axis per launch (the reference's axis
 // order is kept by launching axis 0, 1, 2 in sequence).  One thread per line.
 // mode: 0 always, 1 skip when aborted, 2 only when a non-finite value was found

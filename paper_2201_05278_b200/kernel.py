@@ -244,10 +244,16 @@ class Solver:
             ptr(np.ascontiguousarray(receivers.weight, np.float64))), "fdw_set_receivers")
 
     def add_volume_source(self, source):
-        """kernel.hpp:199-203 -- verification-only forcing; not on the CUDA path."""
+        """kernel.hpp:199-203: dense forcing field (padded shape) times a
+        per-step amplitude, added after the point sources (:439-452)."""
         if len(source.amplitude) < self._time.n_steps:
             raise ValueError("volume source amplitude shorter than run")
-        raise ValueError("volume sources are not supported on the CUDA path")
+        f = np.ascontiguousarray(source.field, dtype=self._dtype)
+        if f.size != int(np.prod(self._shape)):
+            raise ValueError("volume source field shape does not match the padded grid")
+        amp = np.ascontiguousarray(source.amplitude, np.float64)
+        _check(self._ctx, _lib.lib().fdw_add_volume_source(self._ctx, ptr(f), ptr(amp), len(amp), 0),
+               "fdw_add_volume_source")
 
     def set_backend(self, backend, workers: int = 0):
         """kernel.hpp:204-211 -- accepted and ignored (one GPU code path)."""

@@ -119,3 +119,33 @@ def test_variable_density_branch(ndim, order, dtype):
     for _ in range(5):
         assert r.step() == o.step()
         assert same(r.current(), o.current())
+
+
+@pytest.mark.parametrize("ndim,order", [(2, 4), (3, 8)])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_volume_sources(ndim, order, dtype):
+    """Dense modulated sources (kernel.hpp:439-452) after the point sources,
+    two of them in insertion order, plus the amplitude-length check (:199-203)."""
+    ext = (14, 16) if ndim == 2 else (12, 13, 14)
+    pad = tuple(e + order for e in ext)
+    rng = np.random.default_rng(5 + order)
+    vel = (1500 + 3000 * rng.random(pad)).astype(dtype)
+    eta = (20.0 * rng.random(pad)).astype(dtype)
+    sp = [10.0, 12.0, 9.0][:ndim]
+    steps = 12
+    args = (ndim, order, dtype, ext, sp, 0.3 * 9.0 / 4500.0, steps, [[N, D], [X, D], [D, N]], vel, eta)
+    r, o = O.RefSolver(*args), O.OracleSolver(*args)
+    f1 = rng.standard_normal(pad).astype(dtype)
+    f2 = rng.standard_normal(pad).astype(dtype)
+    a1 = np.sin(np.arange(steps + 3) * 0.7)
+    a2 = np.cos(np.arange(steps) * 0.3) * 1e3
+    for s_ in (r, o):
+        s_.add_volume_source(f1, a1)
+        s_.add_volume_source(f2, a2)
+        with pytest.raises(ValueError):
+            s_.add_volume_source(f2, a2[:-1])
+    for _ in range(steps):
+        r.step()
+        o.step()
+        assert same(r.current(), o.current()) and same(r.previous(), o.previous())
+    assert np.abs(o.current()).max() > 0
