@@ -163,11 +163,17 @@ def run_ours(args):
     stream = torch.cuda.Stream()
 
     def make_solver(vel, eta, mats=None):
+        t0 = time.perf_counter()
         s = Solver(w.grid, mats or make_material_model(vel), DampingField(eta=eta), w.spec, w.axis, w.coeffs,
                    device=local, math=math_mode, slab=slab)
+        t1 = time.perf_counter()
         s.set_stream(stream.cuda_stream)
+        t2 = time.perf_counter()
         s.set_sources(w.sources, w.wavelet)
         s.set_receivers(w.receivers)
+        if os.environ.get("FDW_BENCH_DEBUG"):
+            print(f"  make_solver: Solver() {t1 - t0:.3f}, set_stream {t2 - t1:.3f}, maps "
+                  f"{time.perf_counter() - t2:.3f}", file=sys.stderr, flush=True)
         return s
 
     solver = make_solver(w.velocity, w.eta)
@@ -245,12 +251,17 @@ def run_ours(args):
             barrier()
             e0 = time.perf_counter()
             s = make_solver(vel_h, eta_h, mats)
+            e1 = time.perf_counter()
             s.set_host_allocator(pinned_alloc)
             r = s.forward()
             _ = r.seismogram.data, r.snapshots[-1]
+            e2 = time.perf_counter()
             s.close()
             barrier()
             el = time.perf_counter() - e0
+            if os.environ.get("FDW_BENCH_DEBUG"):
+                print(f"e2e iter {it}: {el:.3f} s (ctor {e1 - e0:.3f}, forward {e2 - e1:.3f}, kernel "
+                      f"{r.kernel_seconds:.3f}, close {el - (e2 - e0):.3f})", file=sys.stderr, flush=True)
             if it > 0:  # first call pays graph capture
                 e2e_times.append(el)
         el = statistics.mean(e2e_times)

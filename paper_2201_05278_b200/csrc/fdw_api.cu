@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -18,6 +19,7 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <unordered_map>
@@ -38,6 +40,44 @@ struct ProfileSink {
 };
 
 }  // namespace
+
+// FDW_DEBUG_TIMING=1: host-side phase timings of the setup/teardown calls
+struct PhaseTimer {
+    const char* fn;
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    explicit PhaseTimer(const char* f) : fn(f), on(getenv("FDW_DEBUG_TIMING") != nullptr), t(std::chrono::steady_clock::now()) {}
+    void lap(const char* what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "%s %-14s %8.3f ms\n", fn, what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
+// Pinned host mirrors of Ctrl, recycled across solvers (cudaMallocHost /
+// cudaFreeHost are device-synchronising and slow under memory pressure).
+static std::mutex g_ctrl_mu;
+static std::vector<Ctrl*> g_ctrl_free;
+
+static Ctrl* pinned_ctrl_get() {
+    {
+        std::lock_guard<std::mutex> lk(g_ctrl_mu);
+        if (!g_ctrl_free.empty()) {
+            Ctrl* p = g_ctrl_free.back();
+            g_ctrl_free.pop_back();
+            return p;
+        }
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, sizeof(Ctrl)) != cudaSuccess) return nullptr;
+    return static_cast<Ctrl*>(p);
+}
+
+static void pinned_ctrl_put(Ctrl* p) {
+    std::lock_guard<std::mutex> lk(g_ctrl_mu);
+    g_ctrl_free.push_back(p);
+}
 
 struct fdw_solver {
     fdw_desc d{};
@@ -933,38 +973,66 @@ int pick_zseg(fdw_solver* c, int occ) {
     return best_s;
 }
 
-fdw_status copy_host_to_level(fdw_solver* c, void* dst, const void* src, int on_device) {
-    const size_t row_bytes = (size_t)(c->ndim == 3 ? c->P[2] : c->P[1]) * c->tsize;
-    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (c->ndim == 3) {
-        const size_t plane_bytes_host = (size_t)c->P[1] * row_bytes;
-        for (long long p = 0; p < c->Lz; ++p)
-            CU(cudaMemcpy2DAsync(static_cast<char*>(dst) + ((size_t)p * c->plane + c->base) * c->tsize,
-                                 (size_t)c->ld * c->tsize,
-                                 static_cast<const char*>(src) + (size_t)p * plane_bytes_host, row_bytes,
-                                 row_bytes, (size_t)c->P[1], kind, c->stream));
-    } else {
-        CU(cudaMemcpy2DAsync(static_cast<char*>(dst) + (size_t)c->base * c->tsize, (size_t)c->ld * c->tsize,
-                             src, row_bytes, row_bytes, (size_t)c->P[0], kind, c->stream));
-    }
+// Dense box (nz x nx x ny) <-> pitched device layout, on the device.
+fdw_status launch_box_copy(fdw_solver* c, void* dst, long long d_plane, long long d_row, const void* src,
+                           long long s_plane, long long s_row, long long nz, long long nx, long long ny) {
+    const long long n = nz * nx * ny;
+    if (n <= 0) return FDW_OK;
+    const int tb = 256;
+    const unsigned grid = (unsigned)std::min<long long>((n + tb - 1) / tb, (long long)c->sm_count * 16);
+    if (c->tsize == 4)
+        fdw::box_copy<float><<<grid, tb, 0, c->stream>>>(static_cast<float*>(dst), d_plane, d_row,
+                                                         static_cast<const float*>(src), s_plane, s_row, (int)nz,
+                                                         (int)nx, (int)ny);
+    else
+        fdw::box_copy<double><<<grid, tb, 0, c->stream>>>(static_cast<double*>(dst), d_plane, d_row,
+                                                          static_cast<const double*>(src), s_plane, s_row, (int)nz,
+                                                          (int)nx, (int)ny);
+    CHECK_LAUNCH();
     return FDW_OK;
 }
 
-fdw_status copy_level_to_host(fdw_solver* c, void* dst, const void* src) {
-    const size_t row_bytes = (size_t)(c->ndim == 3 ? c->P[2] : c->P[1]) * c->tsize;
+// Padded box of the local slab in the caller's dense layout: planes, rows, cols
+void padded_box(const fdw_solver* c, long long& nz, long long& nx, long long& ny) {
     if (c->ndim == 3) {
-        const size_t plane_bytes_host = (size_t)c->P[1] * row_bytes;
-        for (long long p = 0; p < c->Lz; ++p)
-            CU(cudaMemcpy2DAsync(static_cast<char*>(dst) + (size_t)p * plane_bytes_host, row_bytes,
-                                 static_cast<const char*>(src) + ((size_t)p * c->plane + c->base) * c->tsize,
-                                 (size_t)c->ld * c->tsize, row_bytes, (size_t)c->P[1],
-                                 cudaMemcpyDeviceToHost, c->stream));
+        nz = c->Lz, nx = c->P[1], ny = c->P[2];
     } else {
-        CU(cudaMemcpy2DAsync(dst, row_bytes, static_cast<const char*>(src) + (size_t)c->base * c->tsize,
-                             (size_t)c->ld * c->tsize, row_bytes, (size_t)c->P[0], cudaMemcpyDeviceToHost,
-                             c->stream));
+        nz = 1, nx = c->P[0], ny = c->P[1];
     }
-    return FDW_OK;
+}
+
+// Host (or device) dense padded array -> pitched level.  A host source goes
+// through ONE contiguous H2D copy into pool memory and is scattered on the
+// device (row-pitched cudaMemcpy2D from host runs at ~half the PCIe rate).
+fdw_status copy_host_to_level(fdw_solver* c, void* dst, const void* src, int on_device) {
+    long long nz, nx, ny;
+    padded_box(c, nz, nx, ny);
+    const size_t bytes = (size_t)(nz * nx * ny) * c->tsize;
+    const void* from = src;
+    void* tmp = nullptr;
+    if (!on_device) {
+        CU(cudaMallocAsync(&tmp, bytes, c->stream));
+        CU(cudaMemcpyAsync(tmp, src, bytes, cudaMemcpyHostToDevice, c->stream));
+        from = tmp;
+    }
+    fdw_status s = launch_box_copy(c, static_cast<char*>(dst) + (size_t)c->base * c->tsize, c->plane, c->ld, from,
+                                   nx * ny, ny, nz, nx, ny);
+    if (tmp) cudaFreeAsync(tmp, c->stream);
+    return s;
+}
+
+// Pitched level -> host dense padded array (one contiguous D2H copy).
+fdw_status copy_level_to_host(fdw_solver* c, void* dst, const void* src) {
+    long long nz, nx, ny;
+    padded_box(c, nz, nx, ny);
+    const size_t bytes = (size_t)(nz * nx * ny) * c->tsize;
+    void* tmp = nullptr;
+    CU(cudaMallocAsync(&tmp, bytes, c->stream));
+    fdw_status s = launch_box_copy(c, tmp, nx * ny, ny, static_cast<const char*>(src) + (size_t)c->base * c->tsize,
+                                   c->plane, c->ld, nz, nx, ny);
+    if (!s) CU(cudaMemcpyAsync(dst, tmp, bytes, cudaMemcpyDeviceToHost, c->stream));
+    cudaFreeAsync(tmp, c->stream);
+    return s;
 }
 
 // Global padded flat index -> device element offset (-1: not on this rank).
@@ -1012,10 +1080,12 @@ bool dropped_target(const fdw_solver* c, unsigned long long flat) {
 
 template <typename P>
 fdw_status dev_upload(fdw_solver* c, P** dst, const std::vector<P>& v) {
-    if (*dst) cudaFree(*dst);
+    // stream-ordered pool memory: a synchronous cudaFree costs a device-wide
+    // sync and, measured on B200, up to seconds while the driver trims
+    if (*dst) cudaFreeAsync(*dst, c->stream);
     *dst = nullptr;
     const size_t n = std::max<size_t>(v.size(), 1);
-    CU(cudaMalloc(dst, n * sizeof(P)));
+    CU(cudaMallocAsync(reinterpret_cast<void**>(dst), n * sizeof(P), c->stream));
     if (!v.empty()) CU(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(P), cudaMemcpyHostToDevice, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     return FDW_OK;
@@ -1169,17 +1239,21 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
         fdw_destroy(c);
         return s;
     };
+    PhaseTimer pt("fdw_create");
     {
         cudaError_t e = cudaSetDevice(d.device);
         if (e != cudaSuccess) {
             fail(c, FDW_ECUDA, "cudaSetDevice(%d): %s", d.device, cudaGetErrorString(e));
             return bail(FDW_ECUDA);
         }
-        cudaDeviceProp prop;
-        if (cudaGetDeviceProperties(&prop, d.device) == cudaSuccess) c->sm_count = prop.multiProcessorCount;
-        if (prop.major < 10) {
-            fail(c, FDW_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a", d.device, prop.major,
-                 prop.minor);
+        // attribute queries, not cudaGetDeviceProperties (which is slow)
+        int major = 0, minor = 0, sms = 0;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d.device);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, d.device);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device) == cudaSuccess && sms > 0)
+            c->sm_count = sms;
+        if (major < 10) {
+            fail(c, FDW_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a", d.device, major, minor);
             return bail(FDW_ECUDA);
         }
     }
@@ -1188,8 +1262,10 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
         fail(c, e == cudaErrorMemoryAllocation ? FDW_ENOMEM : FDW_ECUDA, "%s: %s", what, cudaGetErrorString(e));
         return false;
     };
+    pt.lap("device");
     if (!ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream")) return bail(FDW_ECUDA);
     c->own_stream = true;
+    pt.lap("stream");
     // The four field arrays come from the device's stream-ordered pool with an
     // unlimited release threshold: a process that builds one Solver after
     // another (the reference's one-run-per-Solver usage) reuses the
@@ -1206,9 +1282,14 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
         if (!ck(cudaMallocAsync(p, bytes, c->stream), "cudaMallocAsync(level)")) return bail(FDW_ENOMEM);
         if (!ck(cudaMemsetAsync(*p, 0, bytes, c->stream), "memset")) return bail(FDW_ECUDA);
     }
-    if (!ck(cudaMalloc(&c->ctrl, sizeof(Ctrl)), "cudaMalloc(ctrl)")) return bail(FDW_ENOMEM);
+    if (!ck(cudaMallocAsync(reinterpret_cast<void**>(&c->ctrl), sizeof(Ctrl), c->stream), "cudaMallocAsync(ctrl)"))
+        return bail(FDW_ENOMEM);
     if (!ck(cudaMemsetAsync(c->ctrl, 0, sizeof(Ctrl), c->stream), "memset")) return bail(FDW_ECUDA);
-    if (!ck(cudaMallocHost(&c->h_ctrl, sizeof(Ctrl)), "cudaMallocHost")) return bail(FDW_ENOMEM);
+    if (!(c->h_ctrl = pinned_ctrl_get())) {
+        fail(c, FDW_ENOMEM, "cudaMallocHost(ctrl) failed");
+        return bail(FDW_ENOMEM);
+    }
+    pt.lap("alloc");
 
     // kernel selection
     int variant = d.variant;
@@ -1225,7 +1306,8 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
         c->fused_grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)occ * c->sm_count));
         c->occupancy = occ;
         const size_t n = (size_t)(c->nzl * c->nxl) * sizeof(int);
-        if (!ck(cudaMalloc(&c->d_tmap, n), "cudaMalloc(tmap)")) return bail(FDW_ENOMEM);
+        if (!ck(cudaMallocAsync(reinterpret_cast<void**>(&c->d_tmap), n, c->stream), "cudaMallocAsync(tmap)"))
+            return bail(FDW_ENOMEM);
         if (!ck(cudaMemsetAsync(c->d_tmap, 0, n, c->stream), "memset(tmap)")) return bail(FDW_ECUDA);
     }
     if ((variant == FDW_KERNEL_ZMARCH || variant == FDW_KERNEL_TMA) && (c->ndim != 3 || !zmarch_supported(R)))
@@ -1238,6 +1320,7 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
         }
     }
     c->variant = variant;
+    pt.lap("variant");
     if (variant == FDW_KERNEL_ZMARCH || variant == FDW_KERNEL_TMA) {
         const bool ex = d.math == FDW_MATH_EXACT;
         int occ = 1;
@@ -1274,27 +1357,34 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
             return bail(FDW_ENCCL);
         }
     }
+    pt.lap("kernel_setup");
     if (!ck(cudaStreamSynchronize(c->stream), "sync")) return bail(FDW_ECUDA);
+    pt.lap("sync");
     *out = c;
     return FDW_OK;
 }
 
 fdw_status fdw_destroy(fdw_solver* c) {
     if (!c) return FDW_OK;
+    PhaseTimer pt("fdw_destroy");
+    auto lap = [&](const char* w) { pt.lap(w); };
     cudaSetDevice(c->d.device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    lap("sync");
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    lap("graphs");
     if (c->comm) ncclCommDestroy(c->comm);
     for (void* p : {c->lvl[0], c->lvl[1], c->c2dt2, c->eta, c->grad[0], c->grad[1], c->grad[2]})
         if (p) cudaFreeAsync(p, c->stream);
     for (void* p : c->vs_fields) cudaFreeAsync(p, c->stream);
     for (void* p : {c->d_vs_ptrs, c->d_vs_amp, (void*)c->d_vs_len})
         if (p) cudaFreeAsync(p, c->stream);
-    if (c->stream) cudaStreamSynchronize(c->stream);
     for (void* p : {(void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off, (void*)c->d_ent_w, (void*)c->d_wavelet,
                     (void*)c->d_rec_idx, (void*)c->d_rec_off, (void*)c->d_rec_w, (void*)c->d_seis, (void*)c->d_tmap})
-        if (p) cudaFree(p);
-    if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
+        if (p) cudaFreeAsync(p, c->stream);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    lap("free_async");
+    if (c->h_ctrl) pinned_ctrl_put(c->h_ctrl);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return FDW_OK;
@@ -1321,8 +1411,10 @@ fdw_status fdw_set_medium(fdw_solver* c, const void* velocity, const void* eta, 
     fdw_status s = prologue(c);
     if (s) return s;
     if (!velocity || !eta) return fail(c, FDW_EINVAL, "velocity and eta are required");
+    PhaseTimer pt("fdw_set_medium");
     if ((s = copy_host_to_level(c, c->c2dt2, velocity, on_device))) return s;
     if ((s = copy_host_to_level(c, c->eta, eta, on_device))) return s;
+    pt.lap("enqueue");
     const unsigned long long n = c->level_elems;
     const int tb = 256;
     if (c->tsize == 4)
@@ -1331,6 +1423,7 @@ fdw_status fdw_set_medium(fdw_solver* c, const void* velocity, const void* eta, 
         fdw::c2dt2_kernel<double><<<(unsigned)((n + tb - 1) / tb), tb, 0, c->stream>>>(static_cast<double*>(c->c2dt2), n, c->d.dt);
     CHECK_LAUNCH();
     CU(cudaStreamSynchronize(c->stream));
+    pt.lap("sync");
     c->medium_set = true;
     return FDW_OK;
 }
@@ -1494,13 +1587,13 @@ fdw_status fdw_set_receivers(fdw_solver* c, uint64_t n_points, const uint64_t* o
     if ((s = dev_upload(c, &c->d_rec_idx, ri))) return s;
     if ((s = dev_upload(c, &c->d_rec_off, ro))) return s;
     if ((s = dev_upload(c, &c->d_rec_w, rw))) return s;
-    if (c->d_seis) cudaFree(c->d_seis);
+    if (c->d_seis) cudaFreeAsync(c->d_seis, c->stream);
     c->d_seis = nullptr;
     c->n_rec = (int)n_points;
     c->seis_rows = c->d.n_steps + 1;
     if (n_points) {
         const size_t bytes = (size_t)c->seis_rows * n_points * sizeof(double);
-        CU(cudaMalloc(&c->d_seis, bytes));
+        CU(cudaMallocAsync(reinterpret_cast<void**>(&c->d_seis), bytes, c->stream));
         CU(cudaMemsetAsync(c->d_seis, 0, bytes, c->stream));
         CU(cudaStreamSynchronize(c->stream));
     }
@@ -1545,18 +1638,15 @@ fdw_status fdw_get_extended(fdw_solver* c, void* out) {
     fdw_status s = prologue(c);
     if (s) return s;
     const char* src = static_cast<const char*>(c->lvl[c->cur]);
-    const size_t ts = c->tsize;
-    if (c->ndim == 3) {
-        const size_t row = (size_t)c->nyl * ts;
-        for (long long z = 0; z < c->nzl; ++z)
-            CU(cudaMemcpy2DAsync(static_cast<char*>(out) + (size_t)z * c->nxl * row, row,
-                                 src + (size_t)(c->origin + z * c->plane) * ts, (size_t)c->ld * ts, row,
-                                 (size_t)c->nxl, cudaMemcpyDeviceToHost, c->stream));
-    } else {
-        const size_t row = (size_t)c->nxl * ts;
-        CU(cudaMemcpy2DAsync(out, row, src + (size_t)c->origin * ts, (size_t)c->ld * ts, row, (size_t)c->nzl,
-                             cudaMemcpyDeviceToHost, c->stream));
-    }
+    const long long nz = c->nzl, nx = c->nxl, ny = c->ndim == 3 ? c->nyl : c->nxl;
+    const long long bz = c->ndim == 3 ? nz : 1, bx = c->ndim == 3 ? nx : nz;  // 2D: one plane of Z rows
+    const size_t bytes = (size_t)(bz * bx * ny) * c->tsize;
+    void* tmp = nullptr;
+    CU(cudaMallocAsync(&tmp, bytes, c->stream));
+    s = launch_box_copy(c, tmp, bx * ny, ny, src + (size_t)c->origin * c->tsize, c->plane, c->ld, bz, bx, ny);
+    if (!s) CU(cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, c->stream));
+    cudaFreeAsync(tmp, c->stream);
+    if (s) return s;
     CU(cudaStreamSynchronize(c->stream));
     return FDW_OK;
 }

@@ -1124,6 +1124,22 @@ __global__ void step_advance(Ctrl* ctrl, unsigned long long n) {
 
 // precompute, kernel.hpp:282-285: c2dt2 = T(c * c * dt * dt) in double, in place
 // over the whole allocation (zero padding stays zero).
+// Box copy between the caller's dense layout and the pitched device layout
+// (either direction): nz x nx x ny elements, per-side plane/row strides.
+// Grid-stride; used so host transfers are single contiguous DMA copies.
+template <typename T>
+__global__ void box_copy(T* __restrict__ dst, long long d_plane, long long d_row, const T* __restrict__ src,
+                         long long s_plane, long long s_row, int nz, int nx, int ny) {
+    const long long total = (long long)nz * nx * ny;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(t % ny);
+        const long long r = t / ny;
+        const int x = (int)(r % nx), z = (int)(r / nx);
+        dst[z * d_plane + x * d_row + y] = src[z * s_plane + x * s_row + y];
+    }
+}
+
 template <typename T>
 __global__ void c2dt2_kernel(T* f, unsigned long long n, double dt) {
     const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
