@@ -314,6 +314,8 @@ public:
         if (snap_bytes > snapshot_cap_bytes_)
             throw std::invalid_argument("snapshot storage (" + std::to_string(snap_bytes) +
                                         " bytes) exceeds the configured cap; raise the cap or the stride");
+        // snapshot buffers are written asynchronously: keep them in place
+        result.snapshots.reserve(time_.snapshot_count() + 1);
         refresh_boundary();
         check(fdw_record(ctx_), "fdw_record");
         const std::size_t start = step_index(), n = time_.n_steps, stride = time_.saving_stride;
@@ -322,15 +324,17 @@ public:
         const auto t0 = std::chrono::steady_clock::now();
         std::size_t cur = start;
         const std::size_t end = start + n;
+        // steps and snapshot copies are queued without host syncs; each
+        // snapshot streams out on the copy stream while later steps run
         while (cur < end) {
             std::size_t next = end;
             if (stride != 0) next = std::min(end, (cur / stride + 1) * stride);
             else if (cur < n && n < end) next = n;
-            advance(next - cur, FDW_ADVANCE_RECORD);
+            advance(next - cur, FDW_ADVANCE_RECORD | FDW_ADVANCE_ASYNC);
             cur = next;
-            if (due(cur)) snapshot(result, cur);
+            if (due(cur)) snapshot(result, cur, true);
         }
-        check(fdw_synchronize(ctx_), "fdw_synchronize");
+        wait();
         result.kernel_seconds =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (n_receivers_) {
@@ -386,9 +390,23 @@ private:
             std::fprintf(stderr, "step %zu/%zu\n", step_index(), static_cast<std::size_t>(time_.n_steps));
     }
 
-    void snapshot(ForwardResult<T>& r, std::size_t s) {
+    void wait() {
+        uint64_t bad_step = 0;
+        double bad_max = 0.0;
+        const fdw_status st = fdw_wait(ctx_, &bad_step, &bad_max);
+        if (st == FDW_EINSTABLE) {
+            pull();
+            throw instability_error(bad_step, bad_max);
+        }
+        check(st, "fdw_wait");
+    }
+
+    void snapshot(ForwardResult<T>& r, std::size_t s, bool stream = false) {
         Field<T> out(grid_.ndim, grid_.extended_shape);
-        check(fdw_get_extended(ctx_, out.data()), "fdw_get_extended");
+        if (stream)  // filled by the copy stream; valid after wait()
+            check(fdw_snapshot_async(ctx_, out.data()), "fdw_snapshot_async");
+        else
+            check(fdw_get_extended(ctx_, out.data()), "fdw_get_extended");
         r.snapshots.push_back(std::move(out));
         r.snapshot_steps.push_back(s);
     }

@@ -66,7 +66,11 @@ enum {
 };
 
 /* Advance flags. */
-enum { FDW_ADVANCE_RECORD = 1 /* sample receivers after every step (forward()) */ };
+enum {
+    FDW_ADVANCE_RECORD = 1, /* sample receivers after every step (forward()) */
+    FDW_ADVANCE_ASYNC = 2   /* enqueue only: no host sync; an instability is reported
+                               by the next fdw_wait / state-reading call */
+};
 
 typedef struct fdw_desc {
     int32_t abi_version;     /* FDW_ABI_VERSION */
@@ -169,6 +173,18 @@ fdw_status fdw_record(fdw_solver* ctx);
 fdw_status fdw_advance(fdw_solver* ctx, uint64_t n, uint32_t flags, uint64_t* bad_step,
                        double* bad_max);
 
+/* Waits for the context's compute and copy streams and checks asynchronous
+ * advances: FDW_EINSTABLE with *bad_step / *bad_max as fdw_advance. */
+fdw_status fdw_wait(fdw_solver* ctx, uint64_t* bad_step, double* bad_max);
+
+/* forward()'s strided snapshots, kernel.hpp:305-310 / extract_extended
+ * :313-323, streamed: enqueues a halo-stripped copy of the current level into
+ * out (host, extended shape of this rank) behind the queued steps and returns.
+ * The device copy goes to a ring slot; the host copy runs on a separate copy
+ * stream (pinned destinations directly, others through a pinned bounce slot),
+ * overlapping the following steps.  out is valid after fdw_wait. */
+fdw_status fdw_snapshot_async(fdw_solver* ctx, void* out);
+
 /* Device step counter (Solver<T>::step_index, kernel.hpp:219). */
 fdw_status fdw_step_index(fdw_solver* ctx, uint64_t* step);
 /* Resets the step counter (a fresh forward on the same medium). */
@@ -182,7 +198,8 @@ fdw_status fdw_max_abs(fdw_solver* ctx, double* out);
 fdw_status fdw_download_seismogram(fdw_solver* ctx, void* out, uint64_t rows);
 fdw_status fdw_download_seismogram_f64(fdw_solver* ctx, double* out, uint64_t rows);
 
-/* Waits for all work queued on the context stream. */
+/* Waits for all work queued on the context (compute + copy streams); reports a
+ * pending asynchronous instability like fdw_wait (without the step details). */
 fdw_status fdw_synchronize(fdw_solver* ctx);
 
 /* Profiling: runs n steps with direct launches and CUDA events around every

@@ -17,6 +17,7 @@ FDW_OK, FDW_EINVAL, FDW_ECUDA, FDW_ENCCL, FDW_EINSTABLE, FDW_ENOMEM, FDW_ESTATE 
 FDW_KERNEL_AUTO, FDW_KERNEL_SIMPLE, FDW_KERNEL_ZMARCH, FDW_KERNEL_TMA, FDW_KERNEL_FUSED2D = 0, 1, 2, 3, 4
 FDW_MATH_EXACT, FDW_MATH_FMA = 0, 1
 FDW_ADVANCE_RECORD = 1
+FDW_ADVANCE_ASYNC = 2
 
 
 class fdw_desc(C.Structure):
@@ -59,6 +60,8 @@ _SIGS = {
     "fdw_set_stream": (C.c_int, [_P, _P]),
     "fdw_set_medium": (C.c_int, [_P, _P, _P, C.c_int]),
     "fdw_set_density": (C.c_int, [_P, _P, C.c_int]),
+    "fdw_wait": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
+    "fdw_snapshot_async": (C.c_int, [_P, _P]),
     "fdw_add_volume_source": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_int]),
     "fdw_set_sources": (C.c_int, [_P, C.c_uint64, _P, _P, _P, _P, C.c_uint64]),
     "fdw_set_receivers": (C.c_int, [_P, C.c_uint64, _P, _P, _P]),
@@ -88,10 +91,29 @@ EXPORTED = tuple(_SIGS)
 _lib = None
 
 
+def _preload_nccl():
+    """libfdwave_cuda.so links libnccl.so.2.  In a process that also uses
+    PyTorch, torch's bundled NCCL (newer) must be the one loaded: whichever
+    libnccl.so.2 comes first is shared by soname, and torch fails to import
+    against the older system copy.  So load the bundled one first, globally."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for d in (spec.submodule_search_locations or []) if spec else []:
+            p = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                C.CDLL(p, mode=C.RTLD_GLOBAL)
+                return p
+    except Exception:
+        pass
+    return None
+
+
 def lib():
     """Loads libfdwave_cuda.so once; raises if it is absent (no CPU fallback)."""
     global _lib
     if _lib is None:
+        _preload_nccl()
         if not os.path.exists(LIB_PATH):
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"

@@ -148,6 +148,25 @@ struct fdw_solver {
     // the prev/c2dt2/eta tile box for each level, c2dt2 and eta
     CUtensorMap tm_u[2], tm_p[2], tm_c, tm_e;
     int* d_tmap = nullptr;       // FUSED2D: dense injection-target map over the extended grid
+    // asynchronous advances (FDW_ADVANCE_ASYNC) not yet checked for an abort
+    bool pending = false;
+    unsigned long long pend_start = 0;
+    int pend_cur = 0;
+    // snapshot streaming (fdw_snapshot_async): device pack slots, pinned
+    // bounce slots, a copy stream and per-slot events
+    struct SnapJob {
+        void* dst = nullptr;
+        const void* src = nullptr;
+        size_t bytes = 0;
+    };
+    static constexpr int SNAP_SLOTS = 2;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t snap_packed[SNAP_SLOTS] = {nullptr, nullptr};
+    cudaEvent_t snap_free[SNAP_SLOTS] = {nullptr, nullptr};
+    void* snap_dev[SNAP_SLOTS] = {nullptr, nullptr};
+    void* snap_host[SNAP_SLOTS] = {nullptr, nullptr};
+    size_t snap_bytes = 0;
+    int snap_next = 0;
     int fused_grid = 0;          // FUSED2D: co-resident blocks of the cooperative kernel
 };
 
@@ -1097,6 +1116,45 @@ fdw_status prologue(fdw_solver* c) {
     return FDW_OK;
 }
 
+// Checks the device abort latch after advances (synchronising the stream).
+// On an abort, restores the host bookkeeping to the frozen failing step and
+// returns FDW_EINSTABLE with instability_error's (step, max_abs).
+fdw_status resolve_pending(fdw_solver* c, uint64_t* bad_step, double* bad_max) {
+    if (!c->pending) return FDW_OK;
+    c->pending = false;
+    fdw_status s;
+    if ((s = read_ctrl(c))) return s;
+    if (!c->h_ctrl->abort) return FDW_OK;
+    const unsigned long long done = c->h_ctrl->step - c->pend_start;
+    c->host_step = c->h_ctrl->step;
+    c->cur = c->pend_cur ^ (int)(done & 1);
+    // levels written by executed steps: treat their ghosts as virtual
+    // (settled from the extended values on download)
+    if (c->variant == FDW_KERNEL_TMA) {
+        c->gstate[c->cur] = 1;
+        if (done >= 2) c->gstate[1 - c->cur] = 1;
+    }
+    if (bad_step) *bad_step = c->h_ctrl->bad_step;
+    if (bad_max)
+        *bad_max = c->h_ctrl->kind == 2 ? std::numeric_limits<double>::quiet_NaN()
+                                        : std::numeric_limits<double>::infinity();
+    const unsigned int zero = 0;
+    CU(cudaMemcpyAsync(&c->ctrl->abort, &zero, sizeof(zero), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (c->copy_stream) CU(cudaStreamSynchronize(c->copy_stream));
+    return fail(c, FDW_EINSTABLE, "non-finite wavefield at step %llu; timestep is likely unstable",
+                (unsigned long long)c->h_ctrl->bad_step);
+}
+
+// Entry of every call that reads or replaces device state: pending
+// asynchronous advances are checked first (an instability surfaces here).
+fdw_status enter(fdw_solver* c) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (c->copy_stream) CU(cudaStreamSynchronize(c->copy_stream));
+    return resolve_pending(c, nullptr, nullptr);
+}
+
 }  // namespace
 
 extern "C" {
@@ -1369,8 +1427,16 @@ fdw_status fdw_destroy(fdw_solver* c) {
     PhaseTimer pt("fdw_destroy");
     auto lap = [&](const char* w) { pt.lap(w); };
     cudaSetDevice(c->d.device);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
     lap("sync");
+    for (int k = 0; k < fdw_solver::SNAP_SLOTS; ++k) {
+        if (c->snap_dev[k]) cudaFreeAsync(c->snap_dev[k], c->stream);
+        if (c->snap_host[k]) cudaFreeHost(c->snap_host[k]);
+        if (c->snap_packed[k]) cudaEventDestroy(c->snap_packed[k]);
+        if (c->snap_free[k]) cudaEventDestroy(c->snap_free[k]);
+    }
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     lap("graphs");
     if (c->comm) ncclCommDestroy(c->comm);
@@ -1391,7 +1457,7 @@ fdw_status fdw_destroy(fdw_solver* c) {
 }
 
 fdw_status fdw_set_stream(fdw_solver* c, void* stream) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     CU(cudaStreamSynchronize(c->stream));
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
@@ -1408,7 +1474,7 @@ fdw_status fdw_set_stream(fdw_solver* c, void* stream) {
 }
 
 fdw_status fdw_set_medium(fdw_solver* c, const void* velocity, const void* eta, int on_device) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     if (!velocity || !eta) return fail(c, FDW_EINVAL, "velocity and eta are required");
     PhaseTimer pt("fdw_set_medium");
@@ -1429,7 +1495,7 @@ fdw_status fdw_set_medium(fdw_solver* c, const void* velocity, const void* eta, 
 }
 
 fdw_status fdw_set_density(fdw_solver* c, const void* rho, int on_device) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     if (!rho) return fail(c, FDW_EINVAL, "density is required");
     for (int j = 0; j < c->R; ++j)
@@ -1463,7 +1529,7 @@ fdw_status fdw_set_density(fdw_solver* c, const void* rho, int on_device) {
 
 fdw_status fdw_add_volume_source(fdw_solver* c, const void* field, const double* amplitude, uint64_t n_amp,
                                  int on_device) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     if (!field || (!amplitude && n_amp)) return fail(c, FDW_EINVAL, "volume source field and amplitude required");
     if (n_amp < c->d.n_steps) return fail(c, FDW_EINVAL, "volume source amplitude shorter than run");
@@ -1520,7 +1586,7 @@ fdw_status fdw_add_volume_source(fdw_solver* c, const void* field, const double*
 
 fdw_status fdw_set_sources(fdw_solver* c, uint64_t n_points, const uint64_t* off, const uint64_t* idx,
                            const double* w, const double* wavelet, uint64_t n_samples) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     if (n_points > 0 && n_samples < c->d.n_steps + 1)
         return fail(c, FDW_EINVAL, "wavelet shorter than the time axis");
@@ -1570,7 +1636,7 @@ fdw_status fdw_set_sources(fdw_solver* c, uint64_t n_points, const uint64_t* off
 
 fdw_status fdw_set_receivers(fdw_solver* c, uint64_t n_points, const uint64_t* off, const uint64_t* idx,
                              const double* w) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     std::vector<long long> ri;
     std::vector<unsigned int> ro(1, 0);
@@ -1603,7 +1669,7 @@ fdw_status fdw_set_receivers(fdw_solver* c, uint64_t n_points, const uint64_t* o
 }
 
 fdw_status fdw_set_levels(fdw_solver* c, const void* prev, const void* curr) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     if (prev && (s = copy_host_to_level(c, c->lvl[1 - c->cur], prev, 0))) return s;
     if (curr && (s = copy_host_to_level(c, c->lvl[c->cur], curr, 0))) return s;
@@ -1614,7 +1680,7 @@ fdw_status fdw_set_levels(fdw_solver* c, const void* prev, const void* curr) {
 }
 
 fdw_status fdw_zero_levels(fdw_solver* c) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     const size_t bytes = c->level_elems * c->tsize;
     CU(cudaMemsetAsync(c->lvl[0], 0, bytes, c->stream));
@@ -1624,7 +1690,7 @@ fdw_status fdw_zero_levels(fdw_solver* c) {
 }
 
 fdw_status fdw_get_levels(fdw_solver* c, void* prev, void* curr) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     if (prev && (s = settle_ghosts(c, 1 - c->cur))) return s;
     if (curr && (s = settle_ghosts(c, c->cur))) return s;
@@ -1635,7 +1701,7 @@ fdw_status fdw_get_levels(fdw_solver* c, void* prev, void* curr) {
 }
 
 fdw_status fdw_get_extended(fdw_solver* c, void* out) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     const char* src = static_cast<const char*>(c->lvl[c->cur]);
     const long long nz = c->nzl, nx = c->nxl, ny = c->ndim == 3 ? c->nyl : c->nxl;
@@ -1652,7 +1718,7 @@ fdw_status fdw_get_extended(fdw_solver* c, void* out) {
 }
 
 fdw_status fdw_refresh_boundary(fdw_solver* c) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     if ((s = launch_boundary(c, c->cur, 0))) return s;
     if ((s = launch_halo(c, c->cur))) return s;
@@ -1662,7 +1728,7 @@ fdw_status fdw_refresh_boundary(fdw_solver* c) {
 }
 
 fdw_status fdw_record(fdw_solver* c) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     unsigned long long base = c->host_step;
     CU(cudaMemcpyAsync(&c->ctrl->row_base, &base, sizeof(base), cudaMemcpyHostToDevice, c->stream));
@@ -1677,10 +1743,13 @@ fdw_status fdw_advance(fdw_solver* c, uint64_t n, uint32_t flags, uint64_t* bad_
     if (!c->medium_set) return fail(c, FDW_ESTATE, "fdw_set_medium must be called before fdw_advance");
     const bool record = (flags & FDW_ADVANCE_RECORD) != 0;
     const unsigned long long ci = c->d.check_interval, total = c->d.n_steps;
-    const unsigned long long start = c->host_step;
-    const int cur_start = c->cur;
-    unsigned long long st = start;
-    const unsigned long long end = start + n;
+    if (!c->pending) {
+        c->pending = true;
+        c->pend_start = c->host_step;
+        c->pend_cur = c->cur;
+    }
+    unsigned long long st = c->host_step;
+    const unsigned long long end = st + n;
     while (st < end) {
         unsigned long long nxt = (st / ci + 1) * ci;
         if (total > st) nxt = std::min(nxt, total);
@@ -1689,28 +1758,84 @@ fdw_status fdw_advance(fdw_solver* c, uint64_t n, uint32_t flags, uint64_t* bad_
         if ((s = run_chunk(c, e - st, check, record))) return s;
         st = e;
     }
-    if ((s = read_ctrl(c))) return s;
-    if (c->h_ctrl->abort) {
-        // state is frozen at the failing step; restore host bookkeeping
-        const unsigned long long done = c->h_ctrl->step - start;
-        c->host_step = c->h_ctrl->step;
-        c->cur = cur_start ^ (int)(done & 1);
-        // levels written by executed steps: treat their ghosts as virtual
-        // (settled from the extended values on download)
-        if (c->variant == FDW_KERNEL_TMA) {
-            c->gstate[c->cur] = 1;
-            if (done >= 2) c->gstate[1 - c->cur] = 1;
+    if (flags & FDW_ADVANCE_ASYNC) return FDW_OK;
+    return resolve_pending(c, bad_step, bad_max);
+}
+
+fdw_status fdw_wait(fdw_solver* c, uint64_t* bad_step, double* bad_max) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (c->copy_stream) CU(cudaStreamSynchronize(c->copy_stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return resolve_pending(c, bad_step, bad_max);
+}
+
+namespace {
+void CUDART_CB snap_host_copy(void* p) {
+    auto* j = static_cast<fdw_solver::SnapJob*>(p);
+    std::memcpy(j->dst, j->src, j->bytes);
+    delete j;
+}
+}  // namespace
+
+fdw_status fdw_snapshot_async(fdw_solver* c, void* out) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (!out) return fail(c, FDW_EINVAL, "null snapshot destination");
+    const long long ny = c->ndim == 3 ? c->nyl : c->nxl;
+    const long long bz = c->ndim == 3 ? c->nzl : 1, bx = c->ndim == 3 ? c->nxl : c->nzl;
+    const size_t bytes = (size_t)(bz * bx * ny) * c->tsize;
+    if (!c->copy_stream) {
+        CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (int k = 0; k < fdw_solver::SNAP_SLOTS; ++k) {
+            CU(cudaEventCreateWithFlags(&c->snap_packed[k], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&c->snap_free[k], cudaEventDisableTiming));
+            CU(cudaEventRecord(c->snap_free[k], c->copy_stream));
         }
-        if (bad_step) *bad_step = c->h_ctrl->bad_step;
-        if (bad_max)
-            *bad_max = c->h_ctrl->kind == 2 ? std::numeric_limits<double>::quiet_NaN()
-                                            : std::numeric_limits<double>::infinity();
-        const unsigned int zero = 0;
-        CU(cudaMemcpyAsync(&c->ctrl->abort, &zero, sizeof(zero), cudaMemcpyHostToDevice, c->stream));
-        CU(cudaStreamSynchronize(c->stream));
-        return fail(c, FDW_EINSTABLE, "non-finite wavefield at step %llu; timestep is likely unstable",
-                    (unsigned long long)c->h_ctrl->bad_step);
     }
+    const int k = c->snap_next;
+    if (c->snap_bytes != bytes || !c->snap_dev[k]) {
+        // (re)size every slot once; the copy stream is idle after the sync
+        CU(cudaStreamSynchronize(c->copy_stream));
+        CU(cudaStreamSynchronize(c->stream));
+        for (int q = 0; q < fdw_solver::SNAP_SLOTS; ++q) {
+            if (c->snap_dev[q]) cudaFreeAsync(c->snap_dev[q], c->stream);
+            if (c->snap_host[q]) cudaFreeHost(c->snap_host[q]);
+            c->snap_dev[q] = c->snap_host[q] = nullptr;
+            CU(cudaMallocAsync(&c->snap_dev[q], bytes, c->stream));
+        }
+        c->snap_bytes = bytes;
+    }
+    // pack the extended box of the current level into the slot (compute
+    // stream, after the slot's previous copy-out)
+    CU(cudaStreamWaitEvent(c->stream, c->snap_free[k], 0));
+    const char* src = static_cast<const char*>(c->lvl[c->cur]);
+    if ((s = launch_box_copy(c, c->snap_dev[k], bx * ny, ny, src + (size_t)c->origin * c->tsize, c->plane, c->ld,
+                             bz, bx, ny)))
+        return s;
+    CU(cudaEventRecord(c->snap_packed[k], c->stream));
+    // copy-out on the copy stream: straight into pinned destinations, else
+    // through a pinned bounce slot and a host-side memcpy
+    CU(cudaStreamWaitEvent(c->copy_stream, c->snap_packed[k], 0));
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // clear a benign error from an unregistered pointer
+    if (pinned) {
+        CU(cudaMemcpyAsync(out, c->snap_dev[k], bytes, cudaMemcpyDeviceToHost, c->copy_stream));
+    } else {
+        if (!c->snap_host[k]) CU(cudaMallocHost(&c->snap_host[k], bytes));
+        CU(cudaMemcpyAsync(c->snap_host[k], c->snap_dev[k], bytes, cudaMemcpyDeviceToHost, c->copy_stream));
+        // one job per snapshot (the callback frees it): a slot's previous job
+        // may still be queued when the host reuses the slot
+        auto* job = new fdw_solver::SnapJob{out, c->snap_host[k], bytes};
+        cudaError_t e = cudaLaunchHostFunc(c->copy_stream, snap_host_copy, job);
+        if (e != cudaSuccess) {
+            delete job;
+            return fail(c, FDW_ECUDA, "cudaLaunchHostFunc: %s", cudaGetErrorString(e));
+        }
+    }
+    CU(cudaEventRecord(c->snap_free[k], c->copy_stream));
+    c->snap_next = (k + 1) % fdw_solver::SNAP_SLOTS;
     return FDW_OK;
 }
 
@@ -1721,7 +1846,7 @@ fdw_status fdw_step_index(fdw_solver* c, uint64_t* step) {
 }
 
 fdw_status fdw_set_step_index(fdw_solver* c, uint64_t step) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     unsigned long long v = step;
     CU(cudaMemcpyAsync(&c->ctrl->step, &v, sizeof(v), cudaMemcpyHostToDevice, c->stream));
@@ -1731,7 +1856,7 @@ fdw_status fdw_set_step_index(fdw_solver* c, uint64_t step) {
 }
 
 fdw_status fdw_max_abs(fdw_solver* c, double* out) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     if ((s = launch_health(c, c->cur, 0))) return s;
     if ((s = read_ctrl(c))) return s;
@@ -1748,7 +1873,7 @@ fdw_status fdw_max_abs(fdw_solver* c, double* out) {
 }
 
 fdw_status fdw_download_seismogram_f64(fdw_solver* c, double* out, uint64_t rows) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     if (rows > c->seis_rows) return fail(c, FDW_EINVAL, "rows exceed the seismogram");
     if (c->n_rec == 0 || rows == 0) return FDW_OK;
@@ -1759,7 +1884,7 @@ fdw_status fdw_download_seismogram_f64(fdw_solver* c, double* out, uint64_t rows
 }
 
 fdw_status fdw_download_seismogram(fdw_solver* c, void* out, uint64_t rows) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     if (rows > c->seis_rows) return fail(c, FDW_EINVAL, "rows exceed the seismogram");
     const size_t n = (size_t)rows * c->n_rec;
@@ -1777,12 +1902,13 @@ fdw_status fdw_download_seismogram(fdw_solver* c, void* out, uint64_t rows) {
 fdw_status fdw_synchronize(fdw_solver* c) {
     fdw_status s = prologue(c);
     if (s) return s;
+    if (c->copy_stream) CU(cudaStreamSynchronize(c->copy_stream));
     CU(cudaStreamSynchronize(c->stream));
-    return FDW_OK;
+    return resolve_pending(c, nullptr, nullptr);
 }
 
 fdw_status fdw_profile_steps(fdw_solver* c, uint64_t n, double ms[6]) {
-    fdw_status s = prologue(c);
+    fdw_status s = enter(c);
     if (s) return s;
     if (!c->medium_set) return fail(c, FDW_ESTATE, "fdw_set_medium must be called first");
     ProfileSink sink;

@@ -19,7 +19,7 @@ from typing import List, Optional
 import numpy as np
 
 from . import _lib
-from ._lib import FDW_ADVANCE_RECORD, FDW_EINSTABLE, FDW_EINVAL, FDW_OK, ptr
+from ._lib import FDW_ADVANCE_ASYNC, FDW_ADVANCE_RECORD, FDW_EINSTABLE, FDW_EINVAL, FDW_OK, ptr
 
 
 class BoundaryCondition(enum.IntEnum):  # kernel.hpp:27
@@ -321,6 +321,16 @@ class Solver:
             raise InstabilityError(int(bad_step.value), float(bad_max.value))
         _check(self._ctx, rc, "fdw_advance")
 
+    def _wait(self):
+        bad_step = C.c_uint64()
+        bad_max = C.c_double()
+        rc = _lib.lib().fdw_wait(self._ctx, C.byref(bad_step), C.byref(bad_max))
+        if rc == FDW_EINSTABLE:
+            if self._host_view:
+                self._download()
+            raise InstabilityError(int(bad_step.value), float(bad_max.value))
+        _check(self._ctx, rc, "fdw_wait")
+
     def step(self):
         """kernel.hpp:226-233."""
         self._upload_if_viewed()
@@ -359,13 +369,15 @@ class Solver:
         events.append(end)
         t0 = time.perf_counter()
         cur = start
+        # steps and snapshot copies are queued without host syncs: each
+        # snapshot streams out on the copy stream while later steps run
         for ev in sorted(set(events)):
             if ev > cur:
-                self._advance(ev - cur, FDW_ADVANCE_RECORD)
+                self._advance(ev - cur, FDW_ADVANCE_RECORD | FDW_ADVANCE_ASYNC)
                 cur = ev
             if store(cur) and cur != start:
-                self._snapshot(res, cur)
-        _check(self._ctx, L.fdw_synchronize(self._ctx), "fdw_synchronize")
+                self._snapshot(res, cur, stream=True)
+        self._wait()
         res.kernel_seconds = time.perf_counter() - t0
         if self._n_rec:
             data = self._alloc(((n_total + 1) * self._n_rec,), self._dtype)
@@ -376,9 +388,12 @@ class Solver:
             self._download()
         return res
 
-    def _snapshot(self, res, step):
+    def _snapshot(self, res, step, stream=False):
         out = self._alloc(tuple(self._extended_local()), self._dtype)
-        _check(self._ctx, _lib.lib().fdw_get_extended(self._ctx, ptr(out)), "fdw_get_extended")
+        if stream:  # valid after _wait()
+            _check(self._ctx, _lib.lib().fdw_snapshot_async(self._ctx, ptr(out)), "fdw_snapshot_async")
+        else:
+            _check(self._ctx, _lib.lib().fdw_get_extended(self._ctx, ptr(out)), "fdw_get_extended")
         res.snapshots.append(out)
         res.snapshot_steps.append(step)
 

@@ -91,3 +91,13 @@ def test_create_rejects_bad_descriptors_without_touching_the_gpu():
     d.extended[0], d.extended[1], d.extended[2] = 9, 32, 32  # 9 < 2*4+2
     assert L.fdw_create(C.byref(d), C.byref(C.c_void_p())) == _lib.FDW_EINVAL
     assert b"2*halo+2" in L.fdw_last_error(None)
+
+
+def test_library_then_torch_import_order():
+    """Loading the library before torch must not shadow torch's NCCL."""
+    import subprocess
+    import sys
+    code = ("from paper_2201_05278_b200 import _lib; _lib.lib(); import torch; "
+            "import torch.distributed as d; print(d.is_nccl_available())")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
