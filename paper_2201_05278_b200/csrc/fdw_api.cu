@@ -147,6 +147,7 @@ struct fdw_solver {
     // TMA descriptors (variant FDW_KERNEL_TMA): u-tile box for each level, and
     // the prev/c2dt2/eta tile box for each level, c2dt2 and eta
     CUtensorMap tm_u[2], tm_p[2], tm_c, tm_e;
+    CUtensorMap tm_g[3] = {};    // variable density: grad(rho)/rho tiles
     int* d_tmap = nullptr;       // FUSED2D: dense injection-target map over the extended grid
     // asynchronous advances (FDW_ADVANCE_ASYNC) not yet checked for an abort
     bool pending = false;
@@ -397,12 +398,32 @@ const void* tma_fn() {
 }
 
 template <typename T>
-int tma_smem(int R) {
+int tma_smem(int R, bool vd = false) {
+    if (vd) {
+        switch (R) {
+            case 1: return fdw::TmaShape<T, 1, TMA_BX, 6>::SMEM;
+            case 2: return fdw::TmaShape<T, 2, TMA_BX, 6>::SMEM;
+            default: return fdw::TmaShape<T, 4, TMA_BX, 6>::SMEM;
+        }
+    }
     switch (R) {
         case 1: return fdw::TmaShape<T, 1, TMA_BX>::SMEM;
         case 2: return fdw::TmaShape<T, 2, TMA_BX>::SMEM;
         default: return fdw::TmaShape<T, 4, TMA_BX>::SMEM;
     }
+}
+
+// variable-density TMA sweep (2 CTAs/SM: 6 tiles per plane stage)
+template <typename T>
+const void* tma_vd_kernel(int R, bool ex) {
+#define TKV(RR) \
+    if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 2, true> \
+                           : (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, false, 2, true>;
+    TKV(1)
+    TKV(2)
+    TKV(4)
+#undef TKV
+    return nullptr;
 }
 
 // minb: 2 or 3 resident CTAs requested from ptxas (register cap 128 / 80)
@@ -426,16 +447,22 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a, int src, int dst) {
     dim3 grid((unsigned)((c->nyl + S4::TYW - 1) / S4::TYW), (unsigned)((c->nxl + TMA_BX - 1) / TMA_BX),
               (unsigned)c->zseg);
     const int col_base = (int)(c->base + c->R);
-    const int smem = tma_smem<T>(c->R);
+    const int smem = tma_smem<T>(c->R, c->vd);
+    const CUtensorMap& g0 = c->tm_g[0];
+    const CUtensorMap& g1 = c->tm_g[1];
+    const CUtensorMap& g2 = c->tm_g[2];
     switch (c->R) {
 #define LT(RR)                                                                                          \
     case RR:                                                                                            \
-        if (c->tma_minb == 3)                                                                           \
+        if (c->vd)                                                                                      \
+            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2, true><<<grid, block, smem, c->stream>>>(             \
+                a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);                 \
+        else if (c->tma_minb == 3)                                                                      \
             fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3><<<grid, block, smem, c->stream>>>(                   \
-                a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, col_base);                             \
+                a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);                 \
         else                                                                                            \
             fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2><<<grid, block, smem, c->stream>>>(                   \
-                a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, col_base);                             \
+                a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);                 \
         return true;
         LT(1)
         LT(2)
@@ -589,7 +616,13 @@ template <typename T>
 fdw_status launch_sweep_t(fdw_solver* c, int src, int dst, bool virt) {
     const SweepArgs<T> a = sweep_args<T>(c, src, dst);
     const bool ex = c->d.math == FDW_MATH_EXACT;
-    if (c->variant == FDW_KERNEL_TMA && !virt) {
+    if (c->vd && !(c->variant == FDW_KERNEL_TMA && virt)) {
+        // density terms: the TMA kernel (virtual ghosts) or the element-wise sweep
+        if (ex)
+            launch_simple<T, true>(c, a);
+        else
+            launch_simple<T, false>(c, a);
+    } else if (c->variant == FDW_KERNEL_TMA && !virt) {
         // stored-ghost step (caller-uploaded level): the LDG-fed Z-march
         const bool ok = ex ? launch_zmarch<T, true>(c, a) : launch_zmarch<T, false>(c, a);
         if (!ok) return fail(c, FDW_EINVAL, "zmarch kernel not built for radius %d", c->R);
@@ -1515,11 +1548,29 @@ fdw_status fdw_set_density(fdw_solver* c, const void* rho, int on_device) {
                       : density_grad_t<double>(c, static_cast<const double*>(tmp));
     cudaFreeAsync(tmp, c->stream);
     if (s) return s;
-    // the density terms live in the stored-ghost element-wise sweep: move any
-    // virtual-ghost level to stored ghosts and switch variant
-    if ((s = settle_ghosts(c, 0))) return s;
-    if ((s = settle_ghosts(c, 1))) return s;
-    c->variant = FDW_KERNEL_SIMPLE;
+    if (c->variant == FDW_KERNEL_TMA) {
+        // the TMA sweep streams the three gradient tiles with the others
+        const int pw = c->tsize == 4 ? fdw::TmaShape<float, 1, TMA_BX>::TYW : fdw::TmaShape<double, 1, TMA_BX>::TYW;
+        for (int ax = 0; ax < 3; ++ax)
+            if (!make_map(c, &c->tm_g[ax], c->grad[ax], pw, TMA_BX))
+                return fail(c, FDW_ECUDA, "cuTensorMapEncodeTiled failed (density maps)");
+        const bool ex = c->d.math == FDW_MATH_EXACT;
+        const void* f = c->tsize == 4 ? tma_vd_kernel<float>(c->R, ex) : tma_vd_kernel<double>(c->R, ex);
+        const int smem = c->tsize == 4 ? tma_smem<float>(c->R, true) : tma_smem<double>(c->R, true);
+        CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int occ = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 16 * TMA_BX, smem) != cudaSuccess || occ < 1)
+            occ = 1;
+        c->occupancy = occ;
+        c->zseg = c->d.z_segments > 0 ? c->d.z_segments : pick_zseg(c, occ);
+        if (c->zseg > c->nzl) c->zseg = (int)c->nzl;
+    } else {
+        // the other variants carry the density terms in the stored-ghost
+        // element-wise sweep: move virtual-ghost levels to stored ghosts
+        if ((s = settle_ghosts(c, 0))) return s;
+        if ((s = settle_ghosts(c, 1))) return s;
+        c->variant = FDW_KERNEL_SIMPLE;
+    }
     c->vd = true;
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();

@@ -367,7 +367,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-template <typename T, int R, int BX>
+template <typename T, int R, int BX, int NPA = 3>
 struct TmaShape {
     static constexpr int V = 16 / sizeof(T);
     static constexpr int NTY = 16;
@@ -376,12 +376,12 @@ struct TmaShape {
     static constexpr int UW = TYW + 2 * HY;              // U tile row (elements)
     static constexpr int UH = BX + 2 * R;                // U tile rows
     static constexpr int NU = R + 2;                     // U ring: planes z .. z+R, +1 in flight
-    static constexpr int NP = 2;                         // prev/c2dt2/eta ring
+    static constexpr int NP = 2;                         // prev/c2dt2/eta[/grad x3] ring
     static constexpr int U_BOX = UW * UH * (int)sizeof(T);
     static constexpr int P_BOX = TYW * BX * (int)sizeof(T);
     static constexpr int U_STRIDE = (U_BOX + 127) / 128 * 128;
     static constexpr int P_STRIDE = (P_BOX + 127) / 128 * 128;
-    static constexpr int BAR_OFF = NU * U_STRIDE + NP * 3 * P_STRIDE;
+    static constexpr int BAR_OFF = NU * U_STRIDE + NP * NPA * P_STRIDE;
     static constexpr int SMEM = BAR_OFF + (NU + NP) * 8;
     static constexpr int THREADS = NTY * BX;
 };
@@ -393,12 +393,17 @@ struct TmaShape {
 // mbarriers); the 2R+1 Z neighbours of each thread's V outputs live in a
 // register queue fed from the ring (head = plane z+R).  No per-thread global
 // loads on the hot path; one __syncthreads per plane recycles ring stages.
-template <typename T, int R, int BX, bool EXACT, int MINB>
-__global__ void __launch_bounds__(TmaShape<T, R, BX>::THREADS, MINB)
+// VD (sweep_3d<true>, kernel.hpp:407-417): three more tiles per plane
+// (grad(rho)/rho per axis) and the first-derivative taps on the same operands.
+template <typename T, int R, int BX, bool EXACT, int MINB, bool VD = false>
+__global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
     sweep3d_tma(SweepArgs<T> a, const __grid_constant__ CUtensorMap tu, const __grid_constant__ CUtensorMap tp,
-                const __grid_constant__ CUtensorMap tc, const __grid_constant__ CUtensorMap te, int col_base) {
+                const __grid_constant__ CUtensorMap tc, const __grid_constant__ CUtensorMap te,
+                const __grid_constant__ CUtensorMap tg0, const __grid_constant__ CUtensorMap tg1,
+                const __grid_constant__ CUtensorMap tg2, int col_base) {
     using A = Ar<T, EXACT>;
-    using S = TmaShape<T, R, BX>;
+    constexpr int NPA = VD ? 6 : 3;
+    using S = TmaShape<T, R, BX, NPA>;
     constexpr int V = S::V, NTY = S::NTY, TYW = S::TYW, HY = S::HY, HYV = HY / V, UW = S::UW, NU = S::NU;
     constexpr int THREADS = S::THREADS;
     using VT = Vec<T, V>;
@@ -430,7 +435,7 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX>::THREADS, MINB)
 
     auto u_stage = [&](int k) { return reinterpret_cast<T*>(smem + (k % NU) * S::U_STRIDE); };
     auto p_stage = [&](int k, int which) {
-        return reinterpret_cast<T*>(smem + NU * S::U_STRIDE + ((k & 1) * 3 + which) * S::P_STRIDE);
+        return reinterpret_cast<T*>(smem + NU * S::U_STRIDE + ((k & 1) * NPA + which) * S::P_STRIDE);
     };
     auto issue_u = [&](int k) {  // tile of plane zs + k (mirrored plane beyond a physical Z face)
         unsigned long long* b = &barU[k % NU];
@@ -439,11 +444,16 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX>::THREADS, MINB)
     };
     auto issue_p = [&](int k) {
         unsigned long long* b = &barP[k & 1];
-        mbar_expect_tx(b, 3 * S::P_BOX);
+        mbar_expect_tx(b, NPA * S::P_BOX);
         const int c0 = col_base + ty0, c1 = tx0 + R, c2 = zs + k + R;
         tma_load_3d(p_stage(k, 0), &tp, c0, c1, c2, b);
         tma_load_3d(p_stage(k, 1), &tc, c0, c1, c2, b);
         tma_load_3d(p_stage(k, 2), &te, c0, c1, c2, b);
+        if constexpr (VD) {
+            tma_load_3d(p_stage(k, 3), &tg0, c0, c1, c2, b);
+            tma_load_3d(p_stage(k, 4), &tg1, c0, c1, c2, b);
+            tma_load_3d(p_stage(k, 5), &tg2, c0, c1, c2, b);
+        }
     };
 
     if (tid == 0) {
@@ -534,11 +544,13 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX>::THREADS, MINB)
         }
 
         T lz[V], lx[V], ly[V];
+        T dz[VD ? V : 1], dx[VD ? V : 1], dy[VD ? V : 1];
 #pragma unroll
         for (int e = 0; e < V; ++e) {
             lz[e] = A::mul(a.v[0], q[R].e[e]);
             lx[e] = lz[e];
             ly[e] = lz[e];
+            if constexpr (VD) dz[e] = dx[e] = dy[e] = T(0);
         }
         T w[2 * HY + V];
 #pragma unroll
@@ -558,6 +570,15 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX>::THREADS, MINB)
                 lx[e] = A::add(lx[e], A::mul(vj, A::add(xp.e[e], xm.e[e])));
                 ly[e] = A::add(ly[e], A::mul(vj, A::add(w[HY + e + j], w[HY + e - j])));
             }
+            if constexpr (VD) {  // each accumulator sees the reference's order
+                const T wj = a.w1[j - 1];
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    dz[e] = A::add(dz[e], A::mul(wj, A::sub(q[R + j].e[e], q[R - j].e[e])));
+                    dx[e] = A::add(dx[e], A::mul(wj, A::sub(xp.e[e], xm.e[e])));
+                    dy[e] = A::add(dy[e], A::mul(wj, A::sub(w[HY + e + j], w[HY + e - j])));
+                }
+            }
         }
         const int po = tx * TYW + ty * V;
         const VT pc = *reinterpret_cast<const VT*>(p_stage(it, 0) + po);
@@ -566,8 +587,13 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX>::THREADS, MINB)
         VT res;
 #pragma unroll
         for (int e = 0; e < V; ++e) {
-            const T rhs = A::add(A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1])),
-                                 A::mul(ly[e], a.ih[2]));
+            T rhs = A::add(A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1])), A::mul(ly[e], a.ih[2]));
+            if constexpr (VD) {
+                const T g0 = p_stage(it, 3)[po + e], g1 = p_stage(it, 4)[po + e], g2 = p_stage(it, 5)[po + e];
+                rhs = A::sub(rhs, A::add(A::add(A::mul(A::mul(g0, dz[e]), a.i2h[0]),
+                                                A::mul(A::mul(g1, dx[e]), a.i2h[1])),
+                                         A::mul(A::mul(g2, dy[e]), a.i2h[2])));
+            }
             res.e[e] = time_update<T, EXACT>(rhs, q[R].e[e], cc.e[e], pc.e[e], ec.e[e], a.dt);
         }
         // null-Dirichlet face nodes are forced to +0 (kernel.hpp:87-88)

@@ -6,13 +6,16 @@ from paper_2201_05278_b200 import configs, Solver, make_material_model, DampingF
 from paper_2201_05278_b200._lib import *
 
 _cache = {}
-def run(name, cfg, steps, **kw):
+def run(name, cfg, steps, density=False, **kw):
     key = cfg.name
     if key not in _cache:
         _cache.clear()
         _cache[key] = configs.build_workload(cfg, np.float32)
     w = _cache[key]
-    s = Solver(w.grid, make_material_model(w.velocity), DampingField(eta=w.eta), w.spec, w.axis, w.coeffs, **kw)
+    rho = None
+    if density:  # layered density (g/cm^3) following the velocity, Gardner-like
+        rho = (0.31 * np.power(w.velocity.astype(np.float64), 0.25)).astype(np.float32)
+    s = Solver(w.grid, make_material_model(w.velocity, rho), DampingField(eta=w.eta), w.spec, w.axis, w.coeffs, **kw)
     s.set_sources(w.sources, w.wavelet); s.set_receivers(w.receivers)
     s.advance_raw(100, record=True)  # warm (graph capture)
     pts = w.grid.extended_points()
@@ -27,6 +30,10 @@ def run(name, cfg, steps, **kw):
 if __name__ == "__main__":
     which = sys.argv[1:] or ["all"]
     c4 = configs.overthrust3d(8)
+    if "vd" in which:
+        run("C4-vd", c4, 200, density=True)
+        run("C2-vd", configs.marmousi2d(8), 1600, density=True)
+        sys.exit(0)
     if "2d" in which:
         run("C2", configs.marmousi2d(8), 1600)
         c2 = configs.marmousi2d(8); c2.alpha = 0.0
