@@ -481,8 +481,19 @@ const void* fused2d_fn(int R) {
     return nullptr;
 }
 
+// variable density: exact arithmetic only (FMA mode falls back to SIMPLE)
 template <typename T>
-const void* fused2d_kernel(int R, bool ex) {
+const void* fused2d_vd_fn(int R) {
+#define F2V(RR) \
+    if (R == RR) return (const void*)fdw::step2d_fused<T, RR, true, true>;
+    F2V(1) F2V(2) F2V(3) F2V(4) F2V(5) F2V(6) F2V(7) F2V(8) F2V(9) F2V(10)
+#undef F2V
+    return nullptr;
+}
+
+template <typename T>
+const void* fused2d_kernel(int R, bool ex, bool vd = false) {
+    if (vd) return ex ? fused2d_vd_fn<T>(R) : nullptr;
     return ex ? fused2d_fn<T, true>(R) : fused2d_fn<T, false>(R);
 }
 
@@ -518,13 +529,21 @@ fdw_status launch_fused2d_t(fdw_solver* c, int L, int cur0, bool record, int k0)
     a.n_rec = c->d_seis ? c->n_rec : 0;
     a.n_rows = c->seis_rows;
     a.ctrl = c->ctrl;
+    if (c->vd) {
+        for (int k = 0; k < 2; ++k) {
+            a.grad[k] = static_cast<const T*>(c->grad[k]);
+            a.i2h[k] = static_cast<T>(1.0 / (2.0 * c->d.spacing[k]));
+        }
+        for (int j = 0; j < c->R; ++j) a.w1[j] = static_cast<T>(c->d.coeffs1[j]);
+    }
     {
         const char* dbg = std::getenv("FDW_DEBUG_FUSED");
         a.dbg = dbg ? std::atoi(dbg) : 0;
     }
     int rec = record && c->d_seis ? 1 : 0;
     void* args[] = {&a, &L, &cur0, &rec, &k0};
-    const void* f = fused2d_kernel<T>(c->R, c->d.math == FDW_MATH_EXACT);
+    const void* f = fused2d_kernel<T>(c->R, c->d.math == FDW_MATH_EXACT, c->vd);
+    if (!f) return fail(c, FDW_EINVAL, "fused 2D kernel not built for this configuration");
     CU(cudaLaunchCooperativeKernel(f, dim3((unsigned)c->fused_grid), dim3(256), args, 0, c->stream));
     if (c->capturing)
         ++c->capture_kernels;
@@ -1564,6 +1583,15 @@ fdw_status fdw_set_density(fdw_solver* c, const void* rho, int on_device) {
         c->occupancy = occ;
         c->zseg = c->d.z_segments > 0 ? c->d.z_segments : pick_zseg(c, occ);
         if (c->zseg > c->nzl) c->zseg = (int)c->nzl;
+    } else if (c->variant == FDW_KERNEL_FUSED2D && c->d.math == FDW_MATH_EXACT) {
+        // the cooperative 2D kernel reads the two gradient fields beside
+        // c2dt2/eta; its co-resident grid is re-sized for the VD build
+        const void* f = c->tsize == 4 ? fused2d_kernel<float>(c->R, true, true) : fused2d_kernel<double>(c->R, true, true);
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 256, 0) != cudaSuccess || occ < 1) occ = 1;
+        const long long need = (c->nzl * c->nxl + 255) / 256;
+        c->fused_grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)occ * c->sm_count));
+        c->occupancy = occ;
     } else {
         // the other variants carry the density terms in the stored-ghost
         // element-wise sweep: move virtual-ghost levels to stored ghosts

@@ -659,6 +659,9 @@ struct Fused2DArgs {
     unsigned long long n_rows;
     int dbg;                     // development: bit0 skip sweep, bit1 skip receivers
     Ctrl* ctrl;
+    const T* grad[2];            // variable density: grad(rho)/rho per axis
+    T w1[10];                    // first-derivative weights w_1..w_r
+    T i2h[2];                    // 1/(2h) per axis
 };
 
 template <typename T>
@@ -694,7 +697,7 @@ __device__ void fused2d_receivers(const Fused2DArgs<T>& a, const T* u, unsigned 
     }
 }
 
-template <typename T, int R, bool EXACT>
+template <typename T, int R, bool EXACT, bool VD = false>
 __global__ void __launch_bounds__(256) step2d_fused(Fused2DArgs<T> a, int L, int cur0, int record, int k0) {
     using A = Ar<T, EXACT>;
     constexpr int V = 16 / sizeof(T);
@@ -730,8 +733,12 @@ __global__ void __launch_bounds__(256) step2d_fused(Fused2DArgs<T> a, int L, int
             const long long i0 = a.origin + (long long)z * ld + x0;
             const VT c = *reinterpret_cast<const VT*>(u + i0);
             T lz[V], lx[V], res[V];
+            T dz[VD ? V : 1], dx[VD ? V : 1];
 #pragma unroll
-            for (int e = 0; e < V; ++e) lz[e] = lx[e] = A::mul(a.v[0], c.e[e]);
+            for (int e = 0; e < V; ++e) {
+                lz[e] = lx[e] = A::mul(a.v[0], c.e[e]);
+                if constexpr (VD) dz[e] = dx[e] = T(0);
+            }
             T w[2 * HY + V];
 #pragma unroll
             for (int q = 0; q < 2 * HV + 1; ++q) {
@@ -748,13 +755,28 @@ __global__ void __launch_bounds__(256) step2d_fused(Fused2DArgs<T> a, int L, int
                     lz[e] = A::add(lz[e], A::mul(a.v[j], A::add(zp.e[e], zm.e[e])));
                     lx[e] = A::add(lx[e], A::mul(a.v[j], A::add(w[HY + e + j], w[HY + e - j])));
                 }
+                if constexpr (VD) {  // sweep_2d<true>, kernel.hpp:365-373
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        dz[e] = A::add(dz[e], A::mul(a.w1[j - 1], A::sub(zp.e[e], zm.e[e])));
+                        dx[e] = A::add(dx[e], A::mul(a.w1[j - 1], A::sub(w[HY + e + j], w[HY + e - j])));
+                    }
+                }
             }
             const VT pv = *reinterpret_cast<const VT*>(out + i0);
             const VT cv = ldg16(a.c2dt2 + i0);
             const VT ev = ldg16(a.eta + i0);
+            VT g0v, g1v;
+            if constexpr (VD) {
+                g0v = ldg16(a.grad[0] + i0);
+                g1v = ldg16(a.grad[1] + i0);
+            }
 #pragma unroll
             for (int e = 0; e < V; ++e) {
-                const T rhs = A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1]));
+                T rhs = A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1]));
+                if constexpr (VD)
+                    rhs = A::sub(rhs, A::add(A::mul(A::mul(g0v.e[e], dz[e]), a.i2h[0]),
+                                             A::mul(A::mul(g1v.e[e], dx[e]), a.i2h[1])));
                 res[e] = time_update<T, EXACT>(rhs, c.e[e], cv.e[e], pv.e[e], ev.e[e], a.dt);
             }
             const bool near = z <= R || z >= nz - 1 - R || x0 <= R || x0 + V - 1 >= nx - 1 - R;
