@@ -105,6 +105,7 @@ struct fdw_solver {
     void* eta = nullptr;
     void* grad[3] = {nullptr, nullptr, nullptr};  // variable density: grad(rho)/rho per axis
     bool vd = false;
+    int2* d_ezr = nullptr;  // TMA: eta-zero Z range per tile column
     // volume sources (ModulatedField): device fields, pointer table, amplitudes
     std::vector<void*> vs_fields;
     void* d_vs_ptrs = nullptr;
@@ -325,6 +326,7 @@ SweepArgs<T> sweep_args(fdw_solver* c, int src, int dst) {
         a.gact[0][1] = c->d.rank == c->d.world - 1;
     }
     a.ctrl = c->ctrl;
+    a.ezr = c->d_ezr;
     if (c->vd) {
         a.vd = 1;
         for (int k = 0; k < 3; ++k) {
@@ -1497,7 +1499,7 @@ fdw_status fdw_destroy(fdw_solver* c) {
     for (void* p : c->vs_fields) cudaFreeAsync(p, c->stream);
     for (void* p : {c->d_vs_ptrs, c->d_vs_amp, (void*)c->d_vs_len})
         if (p) cudaFreeAsync(p, c->stream);
-    for (void* p : {(void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off, (void*)c->d_ent_w, (void*)c->d_wavelet,
+    for (void* p : {(void*)c->d_ezr, (void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off, (void*)c->d_ent_w, (void*)c->d_wavelet,
                     (void*)c->d_rec_idx, (void*)c->d_rec_off, (void*)c->d_rec_w, (void*)c->d_seis, (void*)c->d_tmap})
         if (p) cudaFreeAsync(p, c->stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
@@ -1540,6 +1542,22 @@ fdw_status fdw_set_medium(fdw_solver* c, const void* velocity, const void* eta, 
     else
         fdw::c2dt2_kernel<double><<<(unsigned)((n + tb - 1) / tb), tb, 0, c->stream>>>(static_cast<double*>(c->c2dt2), n, c->d.dt);
     CHECK_LAUNCH();
+    if (c->variant == FDW_KERNEL_TMA && std::getenv("FDW_NO_ETA_SKIP") == nullptr) {
+        // per TMA tile column: the planes whose eta tile is all zero
+        const int tyw = c->tsize == 4 ? fdw::TmaShape<float, 1, TMA_BX>::TYW : fdw::TmaShape<double, 1, TMA_BX>::TYW;
+        const int ncy = (int)((c->nyl + tyw - 1) / tyw), ncx = (int)((c->nxl + TMA_BX - 1) / TMA_BX);
+        const size_t ncol = (size_t)ncy * ncx;
+        if (!c->d_ezr) CU(cudaMallocAsync(reinterpret_cast<void**>(&c->d_ezr), ncol * sizeof(int2), c->stream));
+        if (c->tsize == 4)
+            fdw::eta_zero_ranges<float><<<(unsigned)ncol, 256, (size_t)c->nzl, c->stream>>>(
+                static_cast<const float*>(c->eta), c->origin, c->plane, c->ld, (int)c->nzl, (int)c->nxl, (int)c->nyl,
+                TMA_BX, tyw, c->d_ezr);
+        else
+            fdw::eta_zero_ranges<double><<<(unsigned)ncol, 256, (size_t)c->nzl, c->stream>>>(
+                static_cast<const double*>(c->eta), c->origin, c->plane, c->ld, (int)c->nzl, (int)c->nxl,
+                (int)c->nyl, TMA_BX, tyw, c->d_ezr);
+        CHECK_LAUNCH();
+    }
     CU(cudaStreamSynchronize(c->stream));
     pt.lap("sync");
     c->medium_set = true;

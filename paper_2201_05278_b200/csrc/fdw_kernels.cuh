@@ -99,6 +99,9 @@ struct SweepArgs {
     T w1[10];
     T i2h[3];
     int vd;
+    // TMA sweep: per tile column, the Z range [x, y) of planes whose eta tile
+    // is all zero (those planes skip the eta stream); null: none
+    const int2* ezr;
     const Ctrl* ctrl;
 };
 
@@ -432,6 +435,14 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
         return p;
     };
     auto mir = [](int f, T v) { return f == 0 ? T(0) : (f < 0 ? -v : v); };
+    // planes [ez0, ez1) of this column have an all-zero eta tile: no eta
+    // stream there, and the undamped update (om = iop = 1, exact identities)
+    int ez0 = 0, ez1 = 0;
+    if (a.ezr) {
+        const int2 r = a.ezr[blockIdx.y * gridDim.x + blockIdx.x];
+        ez0 = r.x;
+        ez1 = r.y;
+    }
 
     auto u_stage = [&](int k) { return reinterpret_cast<T*>(smem + (k % NU) * S::U_STRIDE); };
     auto p_stage = [&](int k, int which) {
@@ -444,11 +455,12 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
     };
     auto issue_p = [&](int k) {
         unsigned long long* b = &barP[k & 1];
-        mbar_expect_tx(b, NPA * S::P_BOX);
+        const bool skip_e = zs + k >= ez0 && zs + k < ez1;
+        mbar_expect_tx(b, (skip_e ? NPA - 1 : NPA) * S::P_BOX);
         const int c0 = col_base + ty0, c1 = tx0 + R, c2 = zs + k + R;
         tma_load_3d(p_stage(k, 0), &tp, c0, c1, c2, b);
         tma_load_3d(p_stage(k, 1), &tc, c0, c1, c2, b);
-        tma_load_3d(p_stage(k, 2), &te, c0, c1, c2, b);
+        if (!skip_e) tma_load_3d(p_stage(k, 2), &te, c0, c1, c2, b);
         if constexpr (VD) {
             tma_load_3d(p_stage(k, 3), &tg0, c0, c1, c2, b);
             tma_load_3d(p_stage(k, 4), &tg1, c0, c1, c2, b);
@@ -583,10 +595,7 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
         const int po = tx * TYW + ty * V;
         const VT pc = *reinterpret_cast<const VT*>(p_stage(it, 0) + po);
         const VT cc = *reinterpret_cast<const VT*>(p_stage(it, 1) + po);
-        const VT ec = *reinterpret_cast<const VT*>(p_stage(it, 2) + po);
-        VT res;
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
+        auto rhs_of = [&](int e) {
             T rhs = A::add(A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1])), A::mul(ly[e], a.ih[2]));
             if constexpr (VD) {
                 const T g0 = p_stage(it, 3)[po + e], g1 = p_stage(it, 4)[po + e], g2 = p_stage(it, 5)[po + e];
@@ -594,7 +603,18 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
                                                 A::mul(A::mul(g1, dx[e]), a.i2h[1])),
                                          A::mul(A::mul(g2, dy[e]), a.i2h[2])));
             }
-            res.e[e] = time_update<T, EXACT>(rhs, q[R].e[e], cc.e[e], pc.e[e], ec.e[e], a.dt);
+            return rhs;
+        };
+        VT res;
+        if (z >= ez0 && z < ez1) {  // eta == 0: time_update's undamped form
+#pragma unroll
+            for (int e = 0; e < V; ++e)
+                res.e[e] = A::sub(A::add(A::mul(cc.e[e], rhs_of(e)), A::mul(T(2), q[R].e[e])), pc.e[e]);
+        } else {
+            const VT ec = *reinterpret_cast<const VT*>(p_stage(it, 2) + po);
+#pragma unroll
+            for (int e = 0; e < V; ++e)
+                res.e[e] = time_update<T, EXACT>(rhs_of(e), q[R].e[e], cc.e[e], pc.e[e], ec.e[e], a.dt);
         }
         // null-Dirichlet face nodes are forced to +0 (kernel.hpp:87-88)
         if ((zlo && z == 0 && a.gf[0][0] < 0) || (zhi && z == nz - 1 && a.gf[0][1] < 0)) {
@@ -1172,6 +1192,38 @@ __global__ void step_advance(Ctrl* ctrl, unsigned long long n) {
 
 // precompute, kernel.hpp:282-285: c2dt2 = T(c * c * dt * dt) in double, in place
 // over the whole allocation (zero padding stays zero).
+// Eta-zero Z ranges per TMA tile column (BX x TYW outputs): flags[z] = 1 when
+// the column's eta tile on plane z is all zero; thread 0 then keeps the
+// longest run of such planes.  One block per column.
+template <typename T>
+__global__ void eta_zero_ranges(const T* __restrict__ eta, long long origin, long long plane, long long ld, int nz,
+                                int nx, int ny, int bx, int tyw, int2* __restrict__ out) {
+    extern __shared__ unsigned char zflag[];
+    const int col = blockIdx.x;  // = blockIdx.y * gridDim.x + blockIdx.x of the sweep grid
+    const int ncy = (ny + tyw - 1) / tyw;
+    const int x0 = (col / ncy) * bx, y0 = (col % ncy) * tyw;
+    const int w = min(tyw, ny - y0), h = min(bx, nx - x0);
+    for (int z = 0; z < nz; ++z) {
+        int nzv = 0;
+        for (int t = threadIdx.x; t < w * h; t += blockDim.x) {
+            const int xx = x0 + t / w, yy = y0 + t % w;
+            nzv |= eta[origin + (long long)z * plane + (long long)xx * ld + yy] != T(0);
+        }
+        nzv = __syncthreads_or(nzv);
+        if (threadIdx.x == 0) zflag[z] = nzv ? 0 : 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int best0 = 0, best1 = 0, run0 = 0;
+        for (int z = 0; z <= nz; ++z) {
+            if (z < nz && zflag[z]) continue;
+            if (z - run0 > best1 - best0) best0 = run0, best1 = z;
+            run0 = z + 1;
+        }
+        out[col] = make_int2(best0, best1);
+    }
+}
+
 // Box copy between the caller's dense layout and the pitched device layout
 // (either direction): nz x nx x ny elements, per-side plane/row strides.
 // Grid-stride; used so host transfers are single contiguous DMA copies.
