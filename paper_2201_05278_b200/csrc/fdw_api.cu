@@ -327,6 +327,7 @@ SweepArgs<T> sweep_args(fdw_solver* c, int src, int dst) {
     }
     a.ctrl = c->ctrl;
     a.ezr = c->d_ezr;
+    a.negz = static_cast<T>(-0.0);
     if (c->vd) {
         a.vd = 1;
         for (int k = 0; k < 3; ++k) {

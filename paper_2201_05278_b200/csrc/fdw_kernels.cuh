@@ -60,6 +60,28 @@ struct Ar<double, false> {
 
 // 1/(1 + eta dt) and (1 - eta dt) exactly as kernel.hpp:284-287 forms them:
 // double arithmetic on double(eta) * dt, then cast to T.
+// Packed fp32 pairs (sm_100 FADD2 / FFMA2), IEEE round-to-nearest per lane.
+// The exact product is fma(a, b, nz) with nz a RUNTIME -0: ptxas contracts a
+// plain mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under -fmad=false, and
+// a*b + (-0) is exactly RN(a*b) (signed zeros included).
+__device__ __forceinline__ unsigned long long f2u(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 u2f(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b, float2 nz) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(nz)));
+    return u2f(r);
+}
+
 template <typename T>
 __device__ __forceinline__ void damping_factors(T eta, double dt, T& om, T& iop) {
     const double edt = __dmul_rn(static_cast<double>(eta), dt);
@@ -102,6 +124,7 @@ struct SweepArgs {
     // TMA sweep: per tile column, the Z range [x, y) of planes whose eta tile
     // is all zero (those planes skip the eta stream); null: none
     const int2* ezr;
+    T negz;  // -0 (runtime value for the packed exact products)
     const Ctrl* ctrl;
 };
 
@@ -555,66 +578,132 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
             __syncthreads();
         }
 
-        T lz[V], lx[V], ly[V];
-        T dz[VD ? V : 1], dx[VD ? V : 1], dy[VD ? V : 1];
+        constexpr bool PACK = std::is_same<T, float>::value && EXACT && !VD && V == 4;
+        VT res;
+        if constexpr (PACK) {
+            // the same operations in the same order, two lanes per instruction
+            const float2 nz2 = make_float2(a.negz, a.negz);
+            auto pr = [](const VT& v, int p) { return p ? make_float2(v.e[2], v.e[3]) : make_float2(v.e[0], v.e[1]); };
+            float2 lz2[2], lx2[2];
+            T ly[V];
+            const float2 v02 = make_float2(a.v[0], a.v[0]);
 #pragma unroll
-        for (int e = 0; e < V; ++e) {
-            lz[e] = A::mul(a.v[0], q[R].e[e]);
-            lx[e] = lz[e];
-            ly[e] = lz[e];
-            if constexpr (VD) dz[e] = dx[e] = dy[e] = T(0);
-        }
-        T w[2 * HY + V];
-#pragma unroll
-        for (int k = 0; k < 2 * HYV + 1; ++k) {
-            const VT t = *reinterpret_cast<const VT*>(U0 + (R + tx) * UW + ty * V + k * V);
-#pragma unroll
-            for (int e = 0; e < V; ++e) w[k * V + e] = t.e[e];
-        }
-#pragma unroll
-        for (int j = 1; j <= R; ++j) {
-            const VT xp = *reinterpret_cast<const VT*>(U0 + (R + tx + j) * UW + HY + ty * V);
-            const VT xm = *reinterpret_cast<const VT*>(U0 + (R + tx - j) * UW + HY + ty * V);
-            const T vj = a.v[j];
-#pragma unroll
-            for (int e = 0; e < V; ++e) {
-                lz[e] = A::add(lz[e], A::mul(vj, A::add(q[R + j].e[e], q[R - j].e[e])));
-                lx[e] = A::add(lx[e], A::mul(vj, A::add(xp.e[e], xm.e[e])));
-                ly[e] = A::add(ly[e], A::mul(vj, A::add(w[HY + e + j], w[HY + e - j])));
+            for (int p = 0; p < 2; ++p) {
+                lz2[p] = mul2(v02, pr(q[R], p), nz2);
+                lx2[p] = lz2[p];
+                ly[2 * p] = lz2[p].x;
+                ly[2 * p + 1] = lz2[p].y;
             }
-            if constexpr (VD) {  // each accumulator sees the reference's order
-                const T wj = a.w1[j - 1];
+            T w[2 * HY + V];
 #pragma unroll
-                for (int e = 0; e < V; ++e) {
-                    dz[e] = A::add(dz[e], A::mul(wj, A::sub(q[R + j].e[e], q[R - j].e[e])));
-                    dx[e] = A::add(dx[e], A::mul(wj, A::sub(xp.e[e], xm.e[e])));
-                    dy[e] = A::add(dy[e], A::mul(wj, A::sub(w[HY + e + j], w[HY + e - j])));
+            for (int k = 0; k < 2 * HYV + 1; ++k) {
+                const VT t = *reinterpret_cast<const VT*>(U0 + (R + tx) * UW + ty * V + k * V);
+#pragma unroll
+                for (int e = 0; e < V; ++e) w[k * V + e] = t.e[e];
+            }
+#pragma unroll
+            for (int j = 1; j <= R; ++j) {
+                const VT xp = *reinterpret_cast<const VT*>(U0 + (R + tx + j) * UW + HY + ty * V);
+                const VT xm = *reinterpret_cast<const VT*>(U0 + (R + tx - j) * UW + HY + ty * V);
+                const float2 vj2 = make_float2(a.v[j], a.v[j]);
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    lz2[p] = add2(lz2[p], mul2(vj2, add2(pr(q[R + j], p), pr(q[R - j], p)), nz2));
+                    lx2[p] = add2(lx2[p], mul2(vj2, add2(pr(xp, p), pr(xm, p)), nz2));
+                }
+                // ly stays scalar: odd-j Y pairs straddle register pairs (measured slower packed)
+#pragma unroll
+                for (int e = 0; e < V; ++e)
+                    ly[e] = A::add(ly[e], A::mul(a.v[j], A::add(w[HY + e + j], w[HY + e - j])));
+            }
+            const int po = tx * TYW + ty * V;
+            const VT pc = *reinterpret_cast<const VT*>(p_stage(it, 0) + po);
+            const VT cc = *reinterpret_cast<const VT*>(p_stage(it, 1) + po);
+            const float2 ih0 = make_float2(a.ih[0], a.ih[0]), ih1 = make_float2(a.ih[1], a.ih[1]);
+            const float2 ih2 = make_float2(a.ih[2], a.ih[2]), two = make_float2(2.f, 2.f);
+            float2 rhs2[2];
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+                rhs2[p] = add2(add2(mul2(lz2[p], ih0, nz2), mul2(lx2[p], ih1, nz2)),
+                               mul2(make_float2(ly[2 * p], ly[2 * p + 1]), ih2, nz2));
+            if (z >= ez0 && z < ez1) {  // eta == 0: time_update's undamped form
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const float2 r2 = sub2(add2(mul2(pr(cc, p), rhs2[p], nz2), mul2(two, pr(q[R], p), nz2)), pr(pc, p));
+                    res.e[2 * p] = r2.x;
+                    res.e[2 * p + 1] = r2.y;
+                }
+            } else {
+                const VT ec = *reinterpret_cast<const VT*>(p_stage(it, 2) + po);
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    res.e[2 * p] = time_update<T, EXACT>(rhs2[p].x, q[R].e[2 * p], cc.e[2 * p], pc.e[2 * p],
+                                                         ec.e[2 * p], a.dt);
+                    res.e[2 * p + 1] = time_update<T, EXACT>(rhs2[p].y, q[R].e[2 * p + 1], cc.e[2 * p + 1],
+                                                             pc.e[2 * p + 1], ec.e[2 * p + 1], a.dt);
                 }
             }
-        }
-        const int po = tx * TYW + ty * V;
-        const VT pc = *reinterpret_cast<const VT*>(p_stage(it, 0) + po);
-        const VT cc = *reinterpret_cast<const VT*>(p_stage(it, 1) + po);
-        auto rhs_of = [&](int e) {
-            T rhs = A::add(A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1])), A::mul(ly[e], a.ih[2]));
-            if constexpr (VD) {
-                const T g0 = p_stage(it, 3)[po + e], g1 = p_stage(it, 4)[po + e], g2 = p_stage(it, 5)[po + e];
-                rhs = A::sub(rhs, A::add(A::add(A::mul(A::mul(g0, dz[e]), a.i2h[0]),
-                                                A::mul(A::mul(g1, dx[e]), a.i2h[1])),
-                                         A::mul(A::mul(g2, dy[e]), a.i2h[2])));
-            }
-            return rhs;
-        };
-        VT res;
-        if (z >= ez0 && z < ez1) {  // eta == 0: time_update's undamped form
-#pragma unroll
-            for (int e = 0; e < V; ++e)
-                res.e[e] = A::sub(A::add(A::mul(cc.e[e], rhs_of(e)), A::mul(T(2), q[R].e[e])), pc.e[e]);
         } else {
-            const VT ec = *reinterpret_cast<const VT*>(p_stage(it, 2) + po);
-#pragma unroll
-            for (int e = 0; e < V; ++e)
-                res.e[e] = time_update<T, EXACT>(rhs_of(e), q[R].e[e], cc.e[e], pc.e[e], ec.e[e], a.dt);
+            T lz[V], lx[V], ly[V];
+            T dz[VD ? V : 1], dx[VD ? V : 1], dy[VD ? V : 1];
+    #pragma unroll
+            for (int e = 0; e < V; ++e) {
+                lz[e] = A::mul(a.v[0], q[R].e[e]);
+                lx[e] = lz[e];
+                ly[e] = lz[e];
+                if constexpr (VD) dz[e] = dx[e] = dy[e] = T(0);
+            }
+            T w[2 * HY + V];
+    #pragma unroll
+            for (int k = 0; k < 2 * HYV + 1; ++k) {
+                const VT t = *reinterpret_cast<const VT*>(U0 + (R + tx) * UW + ty * V + k * V);
+    #pragma unroll
+                for (int e = 0; e < V; ++e) w[k * V + e] = t.e[e];
+            }
+    #pragma unroll
+            for (int j = 1; j <= R; ++j) {
+                const VT xp = *reinterpret_cast<const VT*>(U0 + (R + tx + j) * UW + HY + ty * V);
+                const VT xm = *reinterpret_cast<const VT*>(U0 + (R + tx - j) * UW + HY + ty * V);
+                const T vj = a.v[j];
+    #pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    lz[e] = A::add(lz[e], A::mul(vj, A::add(q[R + j].e[e], q[R - j].e[e])));
+                    lx[e] = A::add(lx[e], A::mul(vj, A::add(xp.e[e], xm.e[e])));
+                    ly[e] = A::add(ly[e], A::mul(vj, A::add(w[HY + e + j], w[HY + e - j])));
+                }
+                if constexpr (VD) {  // each accumulator sees the reference's order
+                    const T wj = a.w1[j - 1];
+    #pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        dz[e] = A::add(dz[e], A::mul(wj, A::sub(q[R + j].e[e], q[R - j].e[e])));
+                        dx[e] = A::add(dx[e], A::mul(wj, A::sub(xp.e[e], xm.e[e])));
+                        dy[e] = A::add(dy[e], A::mul(wj, A::sub(w[HY + e + j], w[HY + e - j])));
+                    }
+                }
+            }
+            const int po = tx * TYW + ty * V;
+            const VT pc = *reinterpret_cast<const VT*>(p_stage(it, 0) + po);
+            const VT cc = *reinterpret_cast<const VT*>(p_stage(it, 1) + po);
+            auto rhs_of = [&](int e) {
+                T rhs = A::add(A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1])), A::mul(ly[e], a.ih[2]));
+                if constexpr (VD) {
+                    const T g0 = p_stage(it, 3)[po + e], g1 = p_stage(it, 4)[po + e], g2 = p_stage(it, 5)[po + e];
+                    rhs = A::sub(rhs, A::add(A::add(A::mul(A::mul(g0, dz[e]), a.i2h[0]),
+                                                    A::mul(A::mul(g1, dx[e]), a.i2h[1])),
+                                             A::mul(A::mul(g2, dy[e]), a.i2h[2])));
+                }
+                return rhs;
+            };
+            if (z >= ez0 && z < ez1) {  // eta == 0: time_update's undamped form
+    #pragma unroll
+                for (int e = 0; e < V; ++e)
+                    res.e[e] = A::sub(A::add(A::mul(cc.e[e], rhs_of(e)), A::mul(T(2), q[R].e[e])), pc.e[e]);
+            } else {
+                const VT ec = *reinterpret_cast<const VT*>(p_stage(it, 2) + po);
+    #pragma unroll
+                for (int e = 0; e < V; ++e)
+                    res.e[e] = time_update<T, EXACT>(rhs_of(e), q[R].e[e], cc.e[e], pc.e[e], ec.e[e], a.dt);
+            }
         }
         // null-Dirichlet face nodes are forced to +0 (kernel.hpp:87-88)
         if ((zlo && z == 0 && a.gf[0][0] < 0) || (zhi && z == nz - 1 && a.gf[0][1] < 0)) {

@@ -30,6 +30,9 @@ def run(name, cfg, steps, density=False, **kw):
 if __name__ == "__main__":
     which = sys.argv[1:] or ["all"]
     c4 = configs.overthrust3d(8)
+    if "c4only" in which:
+        run("C4-tma", c4, 400)
+        sys.exit(0)
     if "vd" in which:
         run("C4-vd", c4, 200, density=True)
         run("C2-vd", configs.marmousi2d(8), 1600, density=True)
