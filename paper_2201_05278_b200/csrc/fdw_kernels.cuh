@@ -650,6 +650,7 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
         } else {
             T lz[V], lx[V], ly[V];
             T dz[VD ? V : 1], dx[VD ? V : 1], dy[VD ? V : 1];
+            (void)dz, (void)dx, (void)dy;
     #pragma unroll
             for (int e = 0; e < V; ++e) {
                 lz[e] = A::mul(a.v[0], q[R].e[e]);
