@@ -1025,22 +1025,24 @@ fdw_status read_ctrl(fdw_solver* c) {
 // Picks the Z-segment count for the Z-march kernel: fill whole waves of
 // resident CTAs while keeping the 2R-plane queue warm-up small.
 int pick_zseg(fdw_solver* c, int occ) {
+    // Cost model in units of plane-steps of one CTA, fitted on B200 (C4 and C3
+    // sweeps over 4..14 segments): a segment of n planes costs n + 0.2*2R
+    // (queue warm-up); the grid drains at `resident` CTAs; half a CTA of tail
+    // plus half of the idle share of the last partial wave.
     const long long ty = (c->nyl + (64 / (c->tsize / 4)) - 1) / (64 / (c->tsize / 4));
     const long long tx = (c->nxl + 15) / 16;
-    const long long tiles = ty * tx;
+    const double tiles = (double)(ty * tx);
     const double resident = (double)c->sm_count * occ;
-    double best = -1.0;
+    const double warm = 0.2 * 2.0 * c->R;
+    double best = 0.0;
     int best_s = 1;
     for (int s = 1; s <= 16; ++s) {
         if (c->nzl / s < 4 * c->R) break;
-        const double ctas = (double)(tiles * s);
-        const double waves = std::ceil(ctas / resident);
-        const double fill = ctas / (waves * resident);
-        const double warm = 1.0 - 0.2 * (2.0 * c->R * s) / (double)c->nzl;
-        const double balance = std::min(1.0, waves / 6.0);  // many short waves even out SM load
-        const double score = fill * warm * (0.9 + 0.1 * balance);
-        if (score > best + 1e-9) {
-            best = score;
+        const double dur = (double)c->nzl / s + warm;
+        const double waves = tiles * s / resident;
+        const double t = tiles * s * dur / resident + 0.5 * dur + 0.5 * dur * (std::ceil(waves) - waves);
+        if (s == 1 || t < best - 1e-9) {
+            best = t;
             best_s = s;
         }
     }

@@ -30,6 +30,13 @@ def run(name, cfg, steps, density=False, **kw):
 if __name__ == "__main__":
     which = sys.argv[1:] or ["all"]
     c4 = configs.overthrust3d(8)
+    if "zsweep" in which:
+        for zs in (4, 5, 6, 7, 8, 9, 10, 12, 14):
+            run(f"C4-zseg{zs}", c4, 200, z_segments=zs)
+        c3 = configs.overthrust3d(4)
+        for zs in (4, 6, 8, 10):
+            run(f"C3-zseg{zs}", c3, 200, z_segments=zs)
+        sys.exit(0)
     if "c4only" in which:
         run("C4-tma", c4, 400)
         sys.exit(0)
