@@ -151,6 +151,11 @@ struct fdw_solver {
     CUtensorMap tm_g[3] = {};    // variable density: grad(rho)/rho tiles
     int* d_tmap = nullptr;       // FUSED2D: dense injection-target map over the extended grid
     // asynchronous advances (FDW_ADVANCE_ASYNC) not yet checked for an abort
+    // receivers of step k run on a side stream beside the sweep of step k+1
+    // (they only read level k, which step k+2's sweep overwrites)
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork_ev[2] = {nullptr, nullptr};
+    cudaEvent_t rec_ev[2] = {nullptr, nullptr};
     bool pending = false;
     unsigned long long pend_start = 0;
     int pend_cur = 0;
@@ -785,19 +790,23 @@ fdw_status launch_halo(fdw_solver* c, int lv) {
 }
 
 template <typename T>
-fdw_status launch_receivers_t(fdw_solver* c, int lv, int row_add) {
+fdw_status launch_receivers_t(fdw_solver* c, int lv, int row_add, cudaStream_t st) {
     if (c->n_rec == 0 || !c->d_seis) return FDW_OK;
     fdw::receivers_kernel<T><<<(c->n_rec + fdw::REC_WARPS - 1) / fdw::REC_WARPS, 32 * fdw::REC_WARPS, 0,
-                               c->stream>>>(
+                               st>>>(
         static_cast<const T*>(c->lvl[lv]), c->d_rec_idx, c->d_rec_off, c->d_rec_w, c->d_seis, c->n_rec,
         c->seis_rows, row_add, c->ctrl);
     CHECK_LAUNCH();
     return FDW_OK;
 }
 
-fdw_status launch_receivers(fdw_solver* c, int lv, int row_add) {
-    return c->tsize == 4 ? launch_receivers_t<float>(c, lv, row_add) : launch_receivers_t<double>(c, lv, row_add);
+fdw_status launch_receivers(fdw_solver* c, int lv, int row_add, cudaStream_t st = nullptr) {
+    if (!st) st = c->stream;
+    return c->tsize == 4 ? launch_receivers_t<float>(c, lv, row_add, st)
+                         : launch_receivers_t<double>(c, lv, row_add, st);
 }
+
+bool overlap_receivers(const fdw_solver* c) { return c->side && !c->prof && c->n_rec > 0 && c->d_seis; }
 
 // Health reduction over this rank's owned padded planes (global faces keep
 // their ghost planes; internal ghost planes belong to the neighbour).
@@ -907,12 +916,23 @@ bool virtual_step(const fdw_solver* c, int gstate_src) {
 fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
     const int dst = 1 - src;
     fdw_status s;
+    const bool ovl = record && overlap_receivers(c);
+    // this sweep overwrites level `dst`, which step k-2's receivers read
+    if (ovl && k >= 2) CU(cudaStreamWaitEvent(c->stream, c->rec_ev[k & 1], 0));
     { Mark m(c, 0); if ((s = launch_sweep(c, src, dst, virt))) return s; }
     { Mark m(c, 1); if ((s = launch_inject(c, dst, k))) return s; }
     // swap: dst is now the current level
     if (!virt) { Mark m(c, 2); if ((s = launch_faces(c, dst))) return s; }
     if (c->d.world > 1) { Mark m(c, 5); if ((s = launch_halo(c, dst))) return s; }
-    if (record) { Mark m(c, 3); if ((s = launch_receivers(c, dst, k + 1))) return s; }
+    if (record && ovl) {
+        CU(cudaEventRecord(c->fork_ev[k & 1], c->stream));
+        CU(cudaStreamWaitEvent(c->side, c->fork_ev[k & 1], 0));
+        if ((s = launch_receivers(c, dst, k + 1, c->side))) return s;
+        CU(cudaEventRecord(c->rec_ev[k & 1], c->side));
+    } else if (record) {
+        Mark m(c, 3);
+        if ((s = launch_receivers(c, dst, k + 1))) return s;
+    }
     return FDW_OK;
 }
 
@@ -935,6 +955,10 @@ fdw_status enqueue_chunk(fdw_solver* c, unsigned long long L, int cur0, bool che
     } else {
         for (unsigned long long k = 0; k < L; ++k)
             if ((s = enqueue_step(c, (int)k, cur0 ^ (int)(k & 1), record, k == 0 ? first_virt : rest_virt))) return s;
+        if (record && overlap_receivers(c)) {  // join the side stream before the chunk ends
+            CU(cudaStreamWaitEvent(c->stream, c->rec_ev[(L - 1) & 1], 0));
+            if (L >= 2) CU(cudaStreamWaitEvent(c->stream, c->rec_ev[(L - 2) & 1], 0));
+        }
     }
     fdw::step_advance<<<1, 1, 0, c->stream>>>(c->ctrl, L);
     CHECK_LAUNCH();
@@ -1380,6 +1404,11 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
     pt.lap("device");
     if (!ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream")) return bail(FDW_ECUDA);
     c->own_stream = true;
+    if (!ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream")) return bail(FDW_ECUDA);
+    for (int k = 0; k < 2; ++k) {
+        if (!ck(cudaEventCreateWithFlags(&c->fork_ev[k], cudaEventDisableTiming), "event")) return bail(FDW_ECUDA);
+        if (!ck(cudaEventCreateWithFlags(&c->rec_ev[k], cudaEventDisableTiming), "event")) return bail(FDW_ECUDA);
+    }
     pt.lap("stream");
     // The four field arrays come from the device's stream-ordered pool with an
     // unlimited release threshold: a process that builds one Solver after
@@ -1494,6 +1523,12 @@ fdw_status fdw_destroy(fdw_solver* c) {
         if (c->snap_free[k]) cudaEventDestroy(c->snap_free[k]);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->side) cudaStreamSynchronize(c->side);
+    for (int k = 0; k < 2; ++k) {
+        if (c->fork_ev[k]) cudaEventDestroy(c->fork_ev[k]);
+        if (c->rec_ev[k]) cudaEventDestroy(c->rec_ev[k]);
+    }
+    if (c->side) cudaStreamDestroy(c->side);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     lap("graphs");
     if (c->comm) ncclCommDestroy(c->comm);
