@@ -76,6 +76,11 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b) {
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
     return u2f(r);
 }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+    return u2f(r);
+}
 __device__ __forceinline__ float2 mul2(float2 a, float2 b, float2 nz) {
     unsigned long long r;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(nz)));
@@ -582,11 +587,18 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
             __syncthreads();
         }
 
-        constexpr bool PACK = std::is_same<T, float>::value && EXACT && !VD && V == 4;
+        constexpr bool PACK = std::is_same<T, float>::value && !VD && V == 4;
         VT res;
         if constexpr (PACK) {
             // the same operations in the same order, two lanes per instruction
+            // (FMA mode: each multiply-add contracted into FFMA2)
             const float2 nz2 = make_float2(a.negz, a.negz);
+            auto mac2 = [&](float2 acc, float2 x, float2 y) {
+                if constexpr (EXACT)
+                    return add2(acc, mul2(x, y, nz2));
+                else
+                    return fma2(x, y, acc);
+            };
             auto pr = [](const VT& v, int p) { return p ? make_float2(v.e[2], v.e[3]) : make_float2(v.e[0], v.e[1]); };
             float2 lz2[2], lx2[2];
             T ly[V];
@@ -612,8 +624,8 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
                 const float2 vj2 = make_float2(a.v[j], a.v[j]);
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    lz2[p] = add2(lz2[p], mul2(vj2, add2(pr(q[R + j], p), pr(q[R - j], p)), nz2));
-                    lx2[p] = add2(lx2[p], mul2(vj2, add2(pr(xp, p), pr(xm, p)), nz2));
+                    lz2[p] = mac2(lz2[p], vj2, add2(pr(q[R + j], p), pr(q[R - j], p)));
+                    lx2[p] = mac2(lx2[p], vj2, add2(pr(xp, p), pr(xm, p)));
                 }
                 // ly stays scalar: odd-j Y pairs straddle register pairs (measured slower packed)
 #pragma unroll
@@ -628,12 +640,11 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
             float2 rhs2[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p)
-                rhs2[p] = add2(add2(mul2(lz2[p], ih0, nz2), mul2(lx2[p], ih1, nz2)),
-                               mul2(make_float2(ly[2 * p], ly[2 * p + 1]), ih2, nz2));
+                rhs2[p] = mac2(mac2(mul2(lz2[p], ih0, nz2), lx2[p], ih1), make_float2(ly[2 * p], ly[2 * p + 1]), ih2);
             if (z >= ez0 && z < ez1) {  // eta == 0: time_update's undamped form
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    const float2 r2 = sub2(add2(mul2(pr(cc, p), rhs2[p], nz2), mul2(two, pr(q[R], p), nz2)), pr(pc, p));
+                    const float2 r2 = sub2(mac2(mul2(two, pr(q[R], p), nz2), pr(cc, p), rhs2[p]), pr(pc, p));
                     res.e[2 * p] = r2.x;
                     res.e[2 * p + 1] = r2.y;
                 }

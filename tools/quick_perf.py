@@ -39,6 +39,7 @@ if __name__ == "__main__":
         sys.exit(0)
     if "c4only" in which:
         run("C4-tma", c4, 400)
+        run("C4-tma-fma", c4, 400, math=FDW_MATH_FMA)
         sys.exit(0)
     if "vd" in which:
         run("C4-vd", c4, 200, density=True)
