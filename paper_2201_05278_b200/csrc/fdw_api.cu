@@ -156,6 +156,14 @@ struct fdw_solver {
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev[2] = {nullptr, nullptr};
     cudaEvent_t rec_ev[2] = {nullptr, nullptr};
+    // slabs: the first and last Z segments are swept first (compute stream),
+    // their boundary planes exchanged on comm_s while the middle segments are
+    // swept on s2 (halo exchange overlapped with interior compute)
+    cudaStream_t s2 = nullptr, comm_s = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
+    std::vector<long long> h_tgt;             // host copy of the merged targets
+    std::vector<std::vector<double>> h_tw;    // and their entry weights
+    int split_S = -1, n_tgt_a = 0;            // targets reordered: first/last-segment ones first
     bool pending = false;
     unsigned long long pend_start = 0;
     int pend_cur = 0;
@@ -332,6 +340,9 @@ SweepArgs<T> sweep_args(fdw_solver* c, int src, int dst) {
     }
     a.ctrl = c->ctrl;
     a.ezr = c->d_ezr;
+    a.seg_mul = 1;
+    a.seg_add = 0;
+    a.zseg_total = c->zseg;
     a.negz = static_cast<T>(-0.0);
     if (c->vd) {
         a.vd = 1;
@@ -449,11 +460,12 @@ const void* tma_kernel(int R, bool ex, int minb) {
 }
 
 template <typename T, bool EX>
-bool launch_tma(fdw_solver* c, const SweepArgs<T>& a, int src, int dst) {
+bool launch_tma(fdw_solver* c, const SweepArgs<T>& a, int src, int dst, int gz = 0, cudaStream_t st = nullptr) {
     using S4 = fdw::TmaShape<T, 4, TMA_BX>;
+    if (!st) st = c->stream;
     dim3 block(S4::NTY, TMA_BX);
     dim3 grid((unsigned)((c->nyl + S4::TYW - 1) / S4::TYW), (unsigned)((c->nxl + TMA_BX - 1) / TMA_BX),
-              (unsigned)c->zseg);
+              (unsigned)(gz > 0 ? gz : c->zseg));
     const int col_base = (int)(c->base + c->R);
     const int smem = tma_smem<T>(c->R, c->vd);
     const CUtensorMap& g0 = c->tm_g[0];
@@ -463,13 +475,13 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a, int src, int dst) {
 #define LT(RR)                                                                                          \
     case RR:                                                                                            \
         if (c->vd)                                                                                      \
-            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2, true><<<grid, block, smem, c->stream>>>(             \
+            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2, true><<<grid, block, smem, st>>>(                    \
                 a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);                 \
         else if (c->tma_minb == 3)                                                                      \
-            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3><<<grid, block, smem, c->stream>>>(                   \
+            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3><<<grid, block, smem, st>>>(                          \
                 a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);                 \
         else                                                                                            \
-            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2><<<grid, block, smem, c->stream>>>(                   \
+            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2><<<grid, block, smem, st>>>(                          \
                 a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);                 \
         return true;
         LT(1)
@@ -674,12 +686,14 @@ fdw_status launch_sweep(fdw_solver* c, int src, int dst, bool virt) {
 }
 
 template <typename T>
-fdw_status launch_inject_t(fdw_solver* c, int dst, int k) {
-    if (c->n_tgt == 0) return FDW_OK;
+fdw_status launch_inject_t(fdw_solver* c, int dst, int k, int t0 = 0, int cnt = -1, cudaStream_t st = nullptr) {
+    if (cnt < 0) cnt = c->n_tgt - t0;
+    if (cnt <= 0) return FDW_OK;
+    if (!st) st = c->stream;
     const int tb = 128;
-    fdw::inject_kernel<T, true><<<(c->n_tgt + tb - 1) / tb, tb, 0, c->stream>>>(
+    fdw::inject_kernel<T, true><<<(cnt + tb - 1) / tb, tb, 0, st>>>(
         static_cast<T*>(c->lvl[dst]), static_cast<const T*>(c->c2dt2), static_cast<const T*>(c->eta),
-        c->d.dt, c->d_tgt, c->d_ent_off, c->d_ent_w, c->d_wavelet, c->n_wavelet, c->n_tgt, k, c->ctrl);
+        c->d.dt, c->d_tgt + t0, c->d_ent_off + t0, c->d_ent_w, c->d_wavelet, c->n_wavelet, cnt, k, c->ctrl);
     CHECK_LAUNCH();
     return FDW_OK;
 }
@@ -768,22 +782,23 @@ fdw_status launch_boundary(fdw_solver* c, int lv, int mode) {
 ncclDataType_t nccl_type(const fdw_solver* c) { return c->tsize == 4 ? ncclFloat : ncclDouble; }
 
 // Z-halo exchange: R planes per internal face, full padded planes (contiguous).
-fdw_status launch_halo(fdw_solver* c, int lv) {
+fdw_status launch_halo(fdw_solver* c, int lv, cudaStream_t st = nullptr) {
     if (c->d.world <= 1 || c->ndim != 3) return FDW_OK;
+    if (!st) st = c->stream;
     char* f = static_cast<char*>(c->lvl[lv]);
     const size_t n = (size_t)c->R * c->plane;
     const size_t bytes_plane = (size_t)c->plane * c->tsize;
     const int rank = c->d.rank, world = c->d.world;
     NC(ncclGroupStart());
     if (rank > 0) {
-        NC(ncclSend(f + (size_t)c->R * bytes_plane, n, nccl_type(c), rank - 1, c->comm, c->stream));
-        NC(ncclRecv(f, n, nccl_type(c), rank - 1, c->comm, c->stream));
+        NC(ncclSend(f + (size_t)c->R * bytes_plane, n, nccl_type(c), rank - 1, c->comm, st));
+        NC(ncclRecv(f, n, nccl_type(c), rank - 1, c->comm, st));
     }
     if (rank < world - 1) {
         NC(ncclSend(f + (size_t)(c->Lz - 2 * c->R) * bytes_plane, n, nccl_type(c), rank + 1, c->comm,
-                    c->stream));
+                    st));
         NC(ncclRecv(f + (size_t)(c->Lz - c->R) * bytes_plane, n, nccl_type(c), rank + 1, c->comm,
-                    c->stream));
+                    st));
     }
     NC(ncclGroupEnd());
     return FDW_OK;
@@ -913,17 +928,109 @@ bool virtual_step(const fdw_solver* c, int gstate_src) {
     return c->variant == FDW_KERNEL_TMA && gstate_src != 2;
 }
 
+template <typename P>
+fdw_status dev_upload(fdw_solver* c, P** dst, const std::vector<P>& v) {
+    // stream-ordered pool memory: a synchronous cudaFree costs a device-wide
+    // sync and, measured on B200, up to seconds while the driver trims
+    if (*dst) cudaFreeAsync(*dst, c->stream);
+    *dst = nullptr;
+    const size_t n = std::max<size_t>(v.size(), 1);
+    CU(cudaMallocAsync(reinterpret_cast<void**>(dst), n * sizeof(P), c->stream));
+    if (!v.empty()) CU(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(P), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+// Sweep order for slabs: first/last Z segments, then exchange
+// their boundary planes while the middle segments are swept.
+bool split_step(const fdw_solver* c, bool virt) {
+    static const bool off = std::getenv("FDW_NO_HALO_OVERLAP") != nullptr;
+    static const bool force = std::getenv("FDW_FORCE_SPLIT") != nullptr;  // tests on one GPU
+    if (off || !virt || c->prof || c->variant != FDW_KERNEL_TMA || c->ndim != 3 || c->zseg < 3) return false;
+    if (!c->vs_fields.empty() || !c->s2) return false;
+    return c->d.world > 1 || force;
+}
+
+// Orders the targets so that those on planes of the first/last Z segment come
+// first (n_tgt_a of them); per-target entry order is untouched, so the
+// injection is unchanged -- only which launch applies it.
+fdw_status ensure_target_split(fdw_solver* c) {
+    const int S = c->zseg;
+    if (c->split_S == S) return FDW_OK;
+    std::vector<int> order_a, order_b;
+    for (size_t t = 0; t < c->h_tgt.size(); ++t) {
+        const long long z = (c->h_tgt[t] - c->origin) / c->plane;
+        const long long first_end = c->nzl * 1 / S, last_begin = c->nzl * (S - 1) / S;
+        ((z < first_end || z >= last_begin) ? order_a : order_b).push_back((int)t);
+    }
+    std::vector<long long> tg;
+    std::vector<unsigned int> eo(1, 0);
+    std::vector<double> ew;
+    for (const auto* ord : {&order_a, &order_b})
+        for (int t : *ord) {
+            tg.push_back(c->h_tgt[t]);
+            ew.insert(ew.end(), c->h_tw[t].begin(), c->h_tw[t].end());
+            eo.push_back((unsigned int)ew.size());
+        }
+    fdw_status s;
+    if ((s = dev_upload(c, &c->d_tgt, tg))) return s;
+    if ((s = dev_upload(c, &c->d_ent_off, eo))) return s;
+    if ((s = dev_upload(c, &c->d_ent_w, ew))) return s;
+    c->n_tgt_a = (int)order_a.size();
+    c->split_S = S;
+    return FDW_OK;
+}
+
+template <typename T>
+fdw_status enqueue_split_sweep_t(fdw_solver* c, int k, int src, int dst) {
+    const bool ex = c->d.math == FDW_MATH_EXACT;
+    const int S = c->zseg;
+    SweepArgs<T> a = sweep_args<T>(c, src, dst);
+    CU(cudaEventRecord(c->ev_start, c->stream));
+    CU(cudaStreamWaitEvent(c->s2, c->ev_start, 0));
+    // first and last segments (compute stream), then their point sources
+    a.seg_mul = S - 1;
+    a.seg_add = 0;
+    a.zseg_total = S;
+    if (!(ex ? launch_tma<T, true>(c, a, src, dst, 2) : launch_tma<T, false>(c, a, src, dst, 2)))
+        return fail(c, FDW_EINVAL, "TMA kernel not built for radius %d", c->R);
+    CHECK_LAUNCH();
+    fdw_status s;
+    if ((s = launch_inject_t<T>(c, dst, k, 0, c->n_tgt_a, c->stream))) return s;
+    CU(cudaEventRecord(c->ev_a, c->stream));
+    // boundary planes to the neighbours while the middle is swept
+    CU(cudaStreamWaitEvent(c->comm_s, c->ev_a, 0));
+    if ((s = launch_halo(c, dst, c->comm_s))) return s;
+    CU(cudaEventRecord(c->ev_c, c->comm_s));
+    a.seg_mul = 1;
+    a.seg_add = 1;
+    if (!(ex ? launch_tma<T, true>(c, a, src, dst, S - 2, c->s2) : launch_tma<T, false>(c, a, src, dst, S - 2, c->s2)))
+        return fail(c, FDW_EINVAL, "TMA kernel not built for radius %d", c->R);
+    CHECK_LAUNCH();
+    if ((s = launch_inject_t<T>(c, dst, k, c->n_tgt_a, -1, c->s2))) return s;
+    CU(cudaEventRecord(c->ev_b, c->s2));
+    CU(cudaStreamWaitEvent(c->stream, c->ev_b, 0));
+    CU(cudaStreamWaitEvent(c->stream, c->ev_c, 0));
+    return FDW_OK;
+}
+
 fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
     const int dst = 1 - src;
     fdw_status s;
     const bool ovl = record && overlap_receivers(c);
     // this sweep overwrites level `dst`, which step k-2's receivers read
     if (ovl && k >= 2) CU(cudaStreamWaitEvent(c->stream, c->rec_ev[k & 1], 0));
-    { Mark m(c, 0); if ((s = launch_sweep(c, src, dst, virt))) return s; }
-    { Mark m(c, 1); if ((s = launch_inject(c, dst, k))) return s; }
-    // swap: dst is now the current level
-    if (!virt) { Mark m(c, 2); if ((s = launch_faces(c, dst))) return s; }
-    if (c->d.world > 1) { Mark m(c, 5); if ((s = launch_halo(c, dst))) return s; }
+    if (split_step(c, virt)) {
+        // sweep + inject + halo exchange, overlapped (TMA: virtual ghosts, no faces)
+        s = c->tsize == 4 ? enqueue_split_sweep_t<float>(c, k, src, dst) : enqueue_split_sweep_t<double>(c, k, src, dst);
+        if (s) return s;
+    } else {
+        { Mark m(c, 0); if ((s = launch_sweep(c, src, dst, virt))) return s; }
+        { Mark m(c, 1); if ((s = launch_inject(c, dst, k))) return s; }
+        // swap: dst is now the current level
+        if (!virt) { Mark m(c, 2); if ((s = launch_faces(c, dst))) return s; }
+        if (c->d.world > 1) { Mark m(c, 5); if ((s = launch_halo(c, dst))) return s; }
+    }
     if (record && ovl) {
         CU(cudaEventRecord(c->fork_ev[k & 1], c->stream));
         CU(cudaStreamWaitEvent(c->side, c->fork_ev[k & 1], 0));
@@ -973,6 +1080,10 @@ fdw_status enqueue_chunk(fdw_solver* c, unsigned long long L, int cur0, bool che
 }
 
 fdw_status run_chunk(fdw_solver* c, unsigned long long L, bool check, bool record) {
+    if (split_step(c, true)) {  // (uploads; never inside a capture)
+        fdw_status s = ensure_target_split(c);
+        if (s) return s;
+    }
     const int cur0 = c->cur;
     const bool first_virt = virtual_step(c, c->gstate[cur0]);
     const bool rest_virt = virtual_step(c, 0);
@@ -1178,18 +1289,6 @@ bool dropped_target(const fdw_solver* c, unsigned long long flat) {
     return false;
 }
 
-template <typename P>
-fdw_status dev_upload(fdw_solver* c, P** dst, const std::vector<P>& v) {
-    // stream-ordered pool memory: a synchronous cudaFree costs a device-wide
-    // sync and, measured on B200, up to seconds while the driver trims
-    if (*dst) cudaFreeAsync(*dst, c->stream);
-    *dst = nullptr;
-    const size_t n = std::max<size_t>(v.size(), 1);
-    CU(cudaMallocAsync(reinterpret_cast<void**>(dst), n * sizeof(P), c->stream));
-    if (!v.empty()) CU(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(P), cudaMemcpyHostToDevice, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    return FDW_OK;
-}
 
 fdw_status prologue(fdw_solver* c) {
     if (!c) return FDW_EINVAL;
@@ -1405,6 +1504,12 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
     if (!ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream")) return bail(FDW_ECUDA);
     c->own_stream = true;
     if (!ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream")) return bail(FDW_ECUDA);
+    if (d.ndim == 3) {
+        if (!ck(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking), "stream")) return bail(FDW_ECUDA);
+        if (!ck(cudaStreamCreateWithFlags(&c->comm_s, cudaStreamNonBlocking), "stream")) return bail(FDW_ECUDA);
+        for (cudaEvent_t* e : {&c->ev_start, &c->ev_a, &c->ev_b, &c->ev_c})
+            if (!ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event")) return bail(FDW_ECUDA);
+    }
     for (int k = 0; k < 2; ++k) {
         if (!ck(cudaEventCreateWithFlags(&c->fork_ev[k], cudaEventDisableTiming), "event")) return bail(FDW_ECUDA);
         if (!ck(cudaEventCreateWithFlags(&c->rec_ev[k], cudaEventDisableTiming), "event")) return bail(FDW_ECUDA);
@@ -1477,7 +1582,9 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
             if (minb != 2 && minb != 3) {
                 cudaFuncAttributes fa{};
                 const void* f3 = c->tsize == 4 ? tma_kernel<float>(R, ex, 3) : tma_kernel<double>(R, ex, 3);
-                minb = (cudaFuncGetAttributes(&fa, f3) == cudaSuccess && fa.localSizeBytes == 0) ? 3 : 2;
+                // a few spilled bytes (FMA build) cost less than a third CTA per SM
+                // buys (C4 FMA: 0.508 ms at 3 CTAs with 8 B of stack vs 0.578 at 2)
+                minb = (cudaFuncGetAttributes(&fa, f3) == cudaSuccess && fa.localSizeBytes <= 8) ? 3 : 2;
             }
             c->tma_minb = minb;
             const void* f = c->tsize == 4 ? tma_kernel<float>(R, ex, minb) : tma_kernel<double>(R, ex, minb);
@@ -1529,6 +1636,10 @@ fdw_status fdw_destroy(fdw_solver* c) {
         if (c->rec_ev[k]) cudaEventDestroy(c->rec_ev[k]);
     }
     if (c->side) cudaStreamDestroy(c->side);
+    for (cudaEvent_t e : {c->ev_start, c->ev_a, c->ev_b, c->ev_c})
+        if (e) cudaEventDestroy(e);
+    for (cudaStream_t st : {c->s2, c->comm_s})
+        if (st) cudaStreamDestroy(st);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     lap("graphs");
     if (c->comm) ncclCommDestroy(c->comm);
@@ -1747,6 +1858,10 @@ fdw_status fdw_set_sources(fdw_solver* c, uint64_t n_points, const uint64_t* off
         ew.insert(ew.end(), v.begin(), v.end());
         eo.push_back((unsigned int)ew.size());
     }
+    c->h_tgt = tgt;
+    c->h_tw = ws;
+    c->split_S = -1;
+    c->n_tgt_a = 0;
     if ((s = dev_upload(c, &c->d_tgt, tgt))) return s;
     if ((s = dev_upload(c, &c->d_ent_off, eo))) return s;
     if ((s = dev_upload(c, &c->d_ent_w, ew))) return s;

@@ -129,7 +129,13 @@ struct SweepArgs {
     // TMA sweep: per tile column, the Z range [x, y) of planes whose eta tile
     // is all zero (those planes skip the eta stream); null: none
     const int2* ezr;
-    T negz;  // -0 (runtime value for the packed exact products)
+    T negz;
+    // TMA sweep Z segments: CTA z-index b sweeps segment b*seg_mul + seg_add
+    // of zseg_total over [0, nz) (1, 0, gridDim.z: all; S-1, 0, S with
+    // gridDim.z = 2: the first and last; 1, 1, S with gridDim.z = S-2: the
+    // middle).  Used to sweep a slab's boundary planes first and exchange them
+    // while the interior is swept.
+    int seg_mul, seg_add, zseg_total;  // -0 (runtime value for the packed exact products)
     const Ctrl* ctrl;
 };
 
@@ -449,8 +455,9 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
     const int y0 = ty0 + ty * V;
     const int x = tx0 + tx;
     const int nz = a.nz, nx = a.nx, ny = a.ny;
-    const int zs = (int)((long long)nz * blockIdx.z / gridDim.z);
-    const int ze = (int)((long long)nz * (blockIdx.z + 1) / gridDim.z);
+    const int seg = (int)blockIdx.z * a.seg_mul + a.seg_add, nseg = a.zseg_total;
+    const int zs = (int)((long long)nz * seg / nseg);
+    const int ze = (int)((long long)nz * (seg + 1) / nseg);
     const long long plane = a.plane;
     const long long col0 = a.origin + (long long)x * a.ld + y0;
 
