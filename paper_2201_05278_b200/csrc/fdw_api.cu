@@ -948,6 +948,7 @@ bool split_step(const fdw_solver* c, bool virt) {
     static const bool force = std::getenv("FDW_FORCE_SPLIT") != nullptr;  // tests on one GPU
     if (off || !virt || c->prof || c->variant != FDW_KERNEL_TMA || c->ndim != 3 || c->zseg < 3) return false;
     if (!c->vs_fields.empty() || !c->s2) return false;
+    if (c->nzl / c->zseg < c->R) return false;  // the exchanged planes must lie in the end segments
     return c->d.world > 1 || force;
 }
 
