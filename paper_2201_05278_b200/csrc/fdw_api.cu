@@ -861,11 +861,10 @@ fdw_status launch_health_t(fdw_solver* c, int lv, int honor_abort) {
     const unsigned long long P1 = (unsigned long long)c->P[1], P2 = (unsigned long long)c->P[2];
     const int is3d = c->ndim == 3;
     if (!raw) {
-        const long long rows = (long long)ext_planes * ext_rows;
-        const int blocks = (int)std::min<long long>(rows, (long long)c->sm_count * 8);
-        fdw::health_kernel<T><<<blocks, 256, 0, c->stream>>>(u, c->origin_pad, c->ld, c->plane, e_p0, ext_planes, h,
-                                                             ext_rows, h, ext_cols, gp_lo, P1, P2, is3d, c->ctrl,
-                                                             honor_abort, 0);
+        (void)e_p0;
+        fdw::health_scan_ext<T><<<c->sm_count * 8, 256, 0, c->stream>>>(
+            u, c->origin, c->ld, c->plane, ext_planes, ext_rows, ext_cols, h, gp_lo, P1, P2, is3d, c->ctrl,
+            honor_abort);
         CHECK_LAUNCH();
     }
     if (c->d.world > 1) {

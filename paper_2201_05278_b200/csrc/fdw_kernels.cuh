@@ -1274,6 +1274,76 @@ __global__ void health_kernel(const T* __restrict__ u, long long origin_pad, lon
     }
 }
 
+// Extended-point scan of check_health (kernel.hpp:456-467 / max_abs :265-273)
+// as a streaming pass: 16-byte loads (the extended row start is 128-byte
+// aligned), independent loads in flight, max |u| in T (exactly the maximum
+// of the doubles), the first non-finite flat GLOBAL padded index.
+template <typename T>
+__global__ void __launch_bounds__(256) health_scan_ext(const T* __restrict__ u, long long origin, long long ld,
+                                                       long long plane, int nz, int nx, int ny, int h,
+                                                       unsigned long long gplane0, unsigned long long P1,
+                                                       unsigned long long P2, int is3d, Ctrl* ctrl, int honor_abort) {
+    constexpr int V = 16 / sizeof(T);
+    using VT = Vec<T, V>;
+    if (honor_abort && ctrl->abort) return;
+    const int nv = (ny + V - 1) / V;
+    T m = T(0);
+    unsigned long long bad = ~0ull;
+    auto visit = [&](T val, int z, int x, int y) {
+        const T av = fabs(val);
+        if (!isfinite(av)) {
+            const unsigned long long flat =
+                is3d ? ((gplane0 + (unsigned long long)(z + h)) * P1 + (unsigned long long)(x + h)) * P2 + (y + h)
+                     : (unsigned long long)(x + h) * P1 + (y + h);
+            bad = flat < bad ? flat : bad;
+        } else {
+            m = av > m ? av : m;
+        }
+    };
+    // a warp per extended row, lanes over its 16-byte vectors
+    const int lane0 = threadIdx.x & 31;
+    const int nrows = nz * nx;
+    for (int row = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); row < nrows;
+         row += (int)((gridDim.x * blockDim.x) >> 5)) {
+        const int z = row / nx, x = row - z * nx;
+        const T* p = u + origin + (long long)z * plane + (long long)x * ld;
+#pragma unroll 4
+        for (int v = lane0; v < nv; v += 32) {
+            const int y0 = v * V;
+            if (y0 + V <= ny) {
+                const VT t = ldg16(p + y0);
+#pragma unroll
+                for (int e = 0; e < V; ++e) visit(t.e[e], z, x, y0 + e);
+            } else {
+                for (int e = 0; y0 + e < ny; ++e) visit(p[y0 + e], z, x, y0 + e);
+            }
+        }
+    }
+    double md = static_cast<double>(m);
+    for (int o = 16; o > 0; o >>= 1) {
+        const double mo = __shfl_down_sync(0xffffffffu, md, o);
+        const unsigned long long bo = __shfl_down_sync(0xffffffffu, bad, o);
+        md = mo > md ? mo : md;
+        bad = bo < bad ? bo : bad;
+    }
+    __shared__ double sm_m[8];
+    __shared__ unsigned long long sm_b[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        sm_m[wid] = md;
+        sm_b[wid] = bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            md = sm_m[w] > md ? sm_m[w] : md;
+            bad = sm_b[w] < bad ? sm_b[w] : bad;
+        }
+        atomicMax(&ctrl->max_bits, (unsigned long long)__double_as_longlong(md));
+        if (bad != ~0ull) atomicMin(&ctrl->bad_idx, bad);
+    }
+}
+
 __global__ void health_reset(Ctrl* ctrl, int honor_abort) {
     if (honor_abort && ctrl->abort) return;
     ctrl->bad_idx = ~0ull;
