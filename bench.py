@@ -152,7 +152,10 @@ def run_ours(args):
     w = build_workload(cfg, np.float32, rank=rank, world=world)
     setup_s = time.time() - t0
     slab = None
-    if world > 1:
+    # halo transport for N > 1: "peer" (default; the sweep stores the halo
+    # planes straight into the neighbours' levels over NVLink) or "nccl"
+    halo = os.environ.get("FDW_HALO", "peer")
+    if world > 1 and halo == "nccl":
         import ctypes as C
         idbuf = (C.c_ubyte * 128)()
         if rank == 0:
@@ -160,6 +163,8 @@ def run_ours(args):
         obj = [bytes(idbuf)]
         dist.broadcast_object_list(obj, src=0)
         slab = (*w.slab, obj[0])
+    elif world > 1:
+        slab = (*w.slab, None)
     stream = torch.cuda.Stream()
 
     def make_solver(vel, eta, mats=None):
@@ -168,6 +173,9 @@ def run_ours(args):
                    device=local, math=math_mode, slab=slab)
         t1 = time.perf_counter()
         s.set_stream(stream.cuda_stream)
+        if world > 1 and halo != "nccl":
+            from paper_2201_05278_b200 import dist as fdist
+            fdist.link_peers(s)
         t2 = time.perf_counter()
         s.set_sources(w.sources, w.wavelet)
         s.set_receivers(w.receivers)
@@ -301,7 +309,8 @@ def run_ours(args):
             "workload": wname, "name": cfg.name, "extended_shape": list(w.grid.extended_shape[:w.grid.ndim]),
             "space_order": cfg.space_order, "time_steps": n_steps, "points_per_gpu": local_pts,
             "total_points": total_pts, "receivers": w.receivers.n_points, "sources": w.sources.n_points,
-            "math": args.math, "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+            "math": args.math,
+            "parallelism": f"z-slab x{world} ({halo} halo)" if world > 1 else "single GPU",
             "step": "one full forward propagation from rest (inject + record every time step, health every 100)",
             "l2": "inputs exceed L2 (4 fields x ~0.7 GB >> 126 MB); no flush needed",
             "setup_seconds": round(setup_s, 2),

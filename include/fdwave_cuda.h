@@ -93,7 +93,8 @@ typedef struct fdw_desc {
     int32_t z_segments;      /* ZMARCH: Z segments per column (0 -> auto) */
     uint64_t z_begin;        /* first extended Z plane owned by this rank */
     uint64_t z_end;          /* one past the last owned plane */
-    unsigned char nccl_id[128]; /* ncclUniqueId from fdw_nccl_unique_id (world > 1) */
+    unsigned char nccl_id[128]; /* ncclUniqueId from fdw_nccl_unique_id (world > 1); all zero:
+                                   peer transport (fdw_peer_import / fdw_peer_link) */
     double coeffs1[10];      /* StencilCoeffs::first, w_1..w_r (variable density) stencil.hpp:96 */
 } fdw_desc;
 
@@ -215,6 +216,27 @@ fdw_status fdw_launch_count(const fdw_solver* ctx, uint64_t* n);
  * resident CTAs per SM << 16. */
 fdw_status fdw_layout(const fdw_solver* ctx, uint64_t* ld, uint64_t* plane,
                       uint64_t* base, uint64_t* planes, int32_t* variant);
+
+/* ---- peer transport (Z slabs over NVLink / NVSwitch peer memory) ----
+ * A slab context (world > 1) created with an all-zero desc.nccl_id uses no
+ * NCCL: each step's TMA sweep stores its first / last R owned planes straight
+ * into the neighbours' ghost planes through mapped peer memory (the point-source
+ * kernel does the same for targets in those planes; other paths copy the planes
+ * with a push kernel), then one thread per rank signals a step epoch to its
+ * neighbours and waits for theirs (release / acquire at system scope).  The
+ * health reduction (kernel.hpp:456-458 across slabs) goes through the same
+ * per-rank sync blocks.  Replaces the NCCL send/recv of the halo planes.
+ * Every collective call (advance, refresh_boundary, max_abs) must be made on
+ * all ranks, as with NCCL; a neighbour that does not signal within 20 s turns
+ * into FDW_ECUDA instead of a hang. */
+#define FDW_PEER_BLOB_BYTES 512
+/* IPC handles of this rank's levels and sync block plus its slab geometry. */
+fdw_status fdw_peer_export(fdw_solver* ctx, unsigned char out[FDW_PEER_BLOB_BYTES]);
+/* One process per GPU: every rank's export blob in rank order (world x
+ * FDW_PEER_BLOB_BYTES bytes); maps the neighbours' levels and all sync blocks. */
+fdw_status fdw_peer_import(fdw_solver* ctx, const unsigned char* blobs, int32_t world);
+/* One process driving every rank (one thread per context): all[r] = rank r. */
+fdw_status fdw_peer_link(fdw_solver* ctx, fdw_solver* const* all, int32_t world);
 
 /* ---- host-only helpers (no GPU needed) ---- */
 

@@ -84,7 +84,12 @@ _SIGS = {
     "fdw_slab_range": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, _U64P, _U64P]),
     "fdw_owner_of": (C.c_int32, [C.c_uint64, _U64P, C.c_int32, C.c_int32]),
     "fdw_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte * 128)]),
+    "fdw_peer_export": (C.c_int, [_P, _P]),
+    "fdw_peer_import": (C.c_int, [_P, _P, C.c_int32]),
+    "fdw_peer_link": (C.c_int, [_P, _P, C.c_int32]),
 }
+
+FDW_PEER_BLOB_BYTES = 512
 
 EXPORTED = tuple(_SIGS)
 

@@ -25,6 +25,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <unistd.h>
+
 #include "../../include/fdwave_cuda.h"
 #include "fdw_kernels.cuh"
 
@@ -183,6 +185,16 @@ struct fdw_solver {
     size_t snap_bytes = 0;
     int snap_next = 0;
     int fused_grid = 0;          // FUSED2D: co-resident blocks of the cooperative kernel
+    // peer transport (Z slabs, world > 1 with an all-zero nccl_id): halo
+    // planes stored straight into the neighbours' levels over NVLink, step
+    // epochs and the health reduction through per-rank sync blocks
+    bool peer_mode = false;
+    bool peers_ready = false;
+    fdw::PeerSync* psync = nullptr;                        // own sync block (cudaMalloc, IPC-exportable)
+    fdw::PeerSync* peer_sync[fdw::PEER_MAX_WORLD] = {};    // every rank's block, mapped
+    void* peer_lvl[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [lower, upper][level], mapped
+    long long peer_delta[2] = {0, 0};                      // neighbour element = local element + delta
+    std::vector<void*> ipc_mapped;                         // cudaIpcCloseMemHandle on destroy
 };
 
 namespace {
@@ -460,9 +472,16 @@ const void* tma_kernel(int R, bool ex, int minb) {
 }
 
 template <typename T, bool EX>
-bool launch_tma(fdw_solver* c, const SweepArgs<T>& a, int src, int dst, int gz = 0, cudaStream_t st = nullptr) {
+bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst, int gz = 0, cudaStream_t st = nullptr) {
     using S4 = fdw::TmaShape<T, 4, TMA_BX>;
     if (!st) st = c->stream;
+    SweepArgs<T> a = a0;
+    if (c->peer_mode && c->peers_ready) {  // fused halo stores (see enqueue_step)
+        a.peer_lo = static_cast<T*>(c->peer_lvl[0][dst]);
+        a.peer_hi = static_cast<T*>(c->peer_lvl[1][dst]);
+        a.peer_lo_delta = c->peer_delta[0];
+        a.peer_hi_delta = c->peer_delta[1];
+    }
     dim3 block(S4::NTY, TMA_BX);
     dim3 grid((unsigned)((c->nyl + S4::TYW - 1) / S4::TYW), (unsigned)((c->nxl + TMA_BX - 1) / TMA_BX),
               (unsigned)(gz > 0 ? gz : c->zseg));
@@ -691,9 +710,18 @@ fdw_status launch_inject_t(fdw_solver* c, int dst, int k, int t0 = 0, int cnt = 
     if (cnt <= 0) return FDW_OK;
     if (!st) st = c->stream;
     const int tb = 128;
+    fdw::PeerMirror<T> pm;
+    if (c->peer_mode && c->peers_ready) {  // targets in the halo planes reach the neighbour too
+        pm.lo = static_cast<T*>(c->peer_lvl[0][dst]);
+        pm.hi = static_cast<T*>(c->peer_lvl[1][dst]);
+        pm.lo_delta = c->peer_delta[0];
+        pm.hi_delta = c->peer_delta[1];
+        pm.lo_end = c->origin + (long long)c->R * c->plane;
+        pm.hi_begin = c->origin + (c->nzl - c->R) * c->plane;
+    }
     fdw::inject_kernel<T, true><<<(cnt + tb - 1) / tb, tb, 0, st>>>(
         static_cast<T*>(c->lvl[dst]), static_cast<const T*>(c->c2dt2), static_cast<const T*>(c->eta),
-        c->d.dt, c->d_tgt + t0, c->d_ent_off + t0, c->d_ent_w, c->d_wavelet, c->n_wavelet, cnt, k, c->ctrl);
+        c->d.dt, c->d_tgt + t0, c->d_ent_off + t0, c->d_ent_w, c->d_wavelet, c->n_wavelet, cnt, k, c->ctrl, pm);
     CHECK_LAUNCH();
     return FDW_OK;
 }
@@ -781,10 +809,50 @@ fdw_status launch_boundary(fdw_solver* c, int lv, int mode) {
 
 ncclDataType_t nccl_type(const fdw_solver* c) { return c->tsize == 4 ? ncclFloat : ncclDouble; }
 
+fdw::PeerArgs peer_args(fdw_solver* c) {
+    fdw::PeerArgs p{};
+    p.self = c->psync;
+    for (int r = 0; r < fdw::PEER_MAX_WORLD; ++r) p.peer[r] = c->peer_sync[r];
+    p.rank = c->d.rank;
+    p.world = c->d.world;
+    p.ctrl = c->ctrl;
+    return p;
+}
+
+// peer transport: signal this step's halo stores, wait for the neighbours'
+fdw_status launch_peer_sync(fdw_solver* c, cudaStream_t st) {
+    if (!c->peers_ready) return fail(c, FDW_ESTATE, "peer transport: fdw_peer_import / fdw_peer_link first");
+    fdw::peer_halo_sync<<<1, 32, 0, st>>>(peer_args(c));
+    CHECK_LAUNCH();
+    return FDW_OK;
+}
+
+// peer transport: copy the first / last R owned planes of level lv into the
+// neighbours' ghost planes (full padded planes), then synchronise.
+fdw_status launch_peer_push(fdw_solver* c, int lv, cudaStream_t st, bool sync = true) {
+    if (!c->peers_ready) return fail(c, FDW_ESTATE, "peer transport: fdw_peer_import / fdw_peer_link first");
+    const long long n = (long long)c->R * c->plane;
+    const long long lo_src = (long long)c->R * c->plane, hi_src = c->nzl * c->plane;
+    const unsigned grid = (unsigned)std::min<long long>((n / (16 / c->tsize) + 255) / 256, (long long)c->sm_count * 4);
+    if (c->tsize == 4)
+        fdw::peer_push<float><<<grid, 256, 0, st>>>(static_cast<const float*>(c->lvl[lv]),
+                                                     static_cast<float*>(c->peer_lvl[0][lv]),
+                                                     static_cast<float*>(c->peer_lvl[1][lv]), lo_src,
+                                                     c->peer_delta[0], hi_src, c->peer_delta[1], n);
+    else
+        fdw::peer_push<double><<<grid, 256, 0, st>>>(static_cast<const double*>(c->lvl[lv]),
+                                                      static_cast<double*>(c->peer_lvl[0][lv]),
+                                                      static_cast<double*>(c->peer_lvl[1][lv]), lo_src,
+                                                      c->peer_delta[0], hi_src, c->peer_delta[1], n);
+    CHECK_LAUNCH();
+    return sync ? launch_peer_sync(c, st) : FDW_OK;
+}
+
 // Z-halo exchange: R planes per internal face, full padded planes (contiguous).
 fdw_status launch_halo(fdw_solver* c, int lv, cudaStream_t st = nullptr) {
     if (c->d.world <= 1 || c->ndim != 3) return FDW_OK;
     if (!st) st = c->stream;
+    if (c->peer_mode) return launch_peer_push(c, lv, st);
     char* f = static_cast<char*>(c->lvl[lv]);
     const size_t n = (size_t)c->R * c->plane;
     const size_t bytes_plane = (size_t)c->plane * c->tsize;
@@ -867,7 +935,16 @@ fdw_status launch_health_t(fdw_solver* c, int lv, int honor_abort) {
             honor_abort);
         CHECK_LAUNCH();
     }
-    if (c->d.world > 1) {
+    auto peer_reduce = [&]() -> fdw_status {
+        if (!c->peers_ready) return fail(c, FDW_ESTATE, "peer transport: fdw_peer_import / fdw_peer_link first");
+        fdw::peer_allreduce_health<<<1, 32, 0, c->stream>>>(peer_args(c));
+        CHECK_LAUNCH();
+        return FDW_OK;
+    };
+    if (c->d.world > 1 && c->peer_mode) {
+        fdw_status s = peer_reduce();
+        if (s) return s;
+    } else if (c->d.world > 1) {
         NC(ncclAllReduce(&c->ctrl->bad_idx, &c->ctrl->bad_idx, 1, ncclUint64, ncclMin, c->comm, c->stream));
         NC(ncclAllReduce(&c->ctrl->max_bits, &c->ctrl->max_bits, 1, ncclUint64, ncclMax, c->comm, c->stream));
     }
@@ -883,13 +960,21 @@ fdw_status launch_health_t(fdw_solver* c, int lv, int honor_abort) {
                                                              gp_lo, P1, P2, is3d, c->ctrl, honor_abort, raw ? 0 : 1);
         CHECK_LAUNCH();
     }
-    if (c->d.world > 1)
+    if (c->d.world > 1 && c->peer_mode) {
+        fdw_status s = peer_reduce();
+        if (s) return s;
+    } else if (c->d.world > 1) {
         NC(ncclAllReduce(&c->ctrl->bad_idx, &c->ctrl->bad_idx, 1, ncclUint64, ncclMin, c->comm, c->stream));
+    }
     fdw::health_classify<T><<<1, 1, 0, c->stream>>>(u, c->ctrl, c->origin_pad, c->ld, c->plane, gp_lo, gp_hi, P1, P2,
                                                     is3d, honor_abort);
     CHECK_LAUNCH();
-    if (c->d.world > 1)
+    if (c->d.world > 1 && c->peer_mode) {
+        fdw_status s = peer_reduce();
+        if (s) return s;
+    } else if (c->d.world > 1) {
         NC(ncclAllReduce(&c->ctrl->kind, &c->ctrl->kind, 1, ncclUint32, ncclMax, c->comm, c->stream));
+    }
     return FDW_OK;
 }
 
@@ -946,6 +1031,7 @@ bool split_step(const fdw_solver* c, bool virt) {
     static const bool off = std::getenv("FDW_NO_HALO_OVERLAP") != nullptr;
     static const bool force = std::getenv("FDW_FORCE_SPLIT") != nullptr;  // tests on one GPU
     if (off || !virt || c->prof || c->variant != FDW_KERNEL_TMA || c->ndim != 3 || c->zseg < 3) return false;
+    if (c->peer_mode) return false;  // the sweep itself stores the halo planes
     if (!c->vs_fields.empty() || !c->s2) return false;
     if (c->nzl / c->zseg < c->R) return false;  // the exchanged planes must lie in the end segments
     return c->d.world > 1 || force;
@@ -1029,7 +1115,16 @@ fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
         { Mark m(c, 1); if ((s = launch_inject(c, dst, k))) return s; }
         // swap: dst is now the current level
         if (!virt) { Mark m(c, 2); if ((s = launch_faces(c, dst))) return s; }
-        if (c->d.world > 1) { Mark m(c, 5); if ((s = launch_halo(c, dst))) return s; }
+        if (c->d.world > 1 && c->peer_mode) {
+            // the TMA sweep (virtual ghosts) and the point-source kernel stored
+            // the halo planes into the neighbours already; otherwise push them
+            Mark m(c, 5);
+            const bool fused = c->variant == FDW_KERNEL_TMA && virt && c->vs_fields.empty();
+            if ((s = fused ? launch_peer_sync(c, c->stream) : launch_peer_push(c, dst, c->stream))) return s;
+        } else if (c->d.world > 1) {
+            Mark m(c, 5);
+            if ((s = launch_halo(c, dst))) return s;
+        }
     }
     if (record && ovl) {
         CU(cudaEventRecord(c->fork_ev[k & 1], c->stream));
@@ -1305,6 +1400,9 @@ fdw_status resolve_pending(fdw_solver* c, uint64_t* bad_step, double* bad_max) {
     fdw_status s;
     if ((s = read_ctrl(c))) return s;
     if (!c->h_ctrl->abort) return FDW_OK;
+    if (c->h_ctrl->peer_err)
+        return fail(c, FDW_ECUDA, "peer transport: a neighbour did not signal within 20 s (rank %d of %d)",
+                    c->d.rank, c->d.world);
     const unsigned long long done = c->h_ctrl->step - c->pend_start;
     c->host_step = c->h_ctrl->step;
     c->cur = c->pend_cur ^ (int)(done & 1);
@@ -1388,6 +1486,117 @@ int32_t fdw_owner_of(uint64_t flat, const uint64_t ext[3], int32_t halo, int32_t
         if (fdw_slab_range(ext[0], world, r, &b, &e) == FDW_OK && (uint64_t)z >= b && (uint64_t)z < e) return r;
     }
     return -1;
+}
+
+namespace {
+struct PeerBlob {
+    uint32_t magic;
+    int32_t rank, world, tsize, R, device;
+    int64_t ld, plane, nzl, origin, pid;
+    cudaIpcMemHandle_t lvl[2];
+    cudaIpcMemHandle_t sync;
+};
+static_assert(sizeof(PeerBlob) <= FDW_PEER_BLOB_BYTES, "peer blob size");
+constexpr uint32_t PEER_MAGIC = 0x50574446u;  // "FDWP"
+
+// Mapping of the neighbours' levels: neighbour element = local element + delta.
+// Lower neighbour: local plane z in [0, R) is its plane nzl_lo + z.  Upper
+// neighbour: local plane z in [nzl - R, nzl) is its plane z - nzl.
+fdw_status peer_geometry(fdw_solver* c, int s, long long ld, long long plane, long long nzl, long long origin,
+                         int tsize, int R) {
+    if (ld != c->ld || plane != c->plane || tsize != c->tsize || R != c->R)
+        return fail(c, FDW_EINVAL, "peer rank %d: slab layout differs (ld %lld/%lld, plane %lld/%lld)", s, ld,
+                    c->ld, plane, c->plane);
+    if (nzl < c->R) return fail(c, FDW_EINVAL, "peer rank %d owns fewer than R planes", s);
+    if (s == c->d.rank - 1) c->peer_delta[0] = origin + nzl * plane - c->origin;
+    if (s == c->d.rank + 1) c->peer_delta[1] = origin - c->nzl * plane - c->origin;
+    return FDW_OK;
+}
+}  // namespace
+
+fdw_status fdw_peer_export(fdw_solver* c, unsigned char out[FDW_PEER_BLOB_BYTES]) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (!out) return fail(c, FDW_EINVAL, "null output");
+    if (!c->peer_mode) return fail(c, FDW_EINVAL, "not a peer-transport slab context");
+    PeerBlob b{};
+    b.magic = PEER_MAGIC;
+    b.rank = c->d.rank;
+    b.world = c->d.world;
+    b.tsize = c->tsize;
+    b.R = c->R;
+    b.device = c->d.device;
+    b.ld = c->ld;
+    b.plane = c->plane;
+    b.nzl = c->nzl;
+    b.origin = c->origin;
+    b.pid = (int64_t)getpid();
+    for (int l = 0; l < 2; ++l) CU(cudaIpcGetMemHandle(&b.lvl[l], c->lvl[l]));
+    CU(cudaIpcGetMemHandle(&b.sync, c->psync));
+    std::memset(out, 0, FDW_PEER_BLOB_BYTES);
+    std::memcpy(out, &b, sizeof(b));
+    return FDW_OK;
+}
+
+fdw_status fdw_peer_import(fdw_solver* c, const unsigned char* blobs, int32_t world) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (!c->peer_mode) return fail(c, FDW_EINVAL, "not a peer-transport slab context");
+    if (!blobs || world != c->d.world) return fail(c, FDW_EINVAL, "need one blob per rank (%d)", c->d.world);
+    if (c->peers_ready) return fail(c, FDW_ESTATE, "peers already imported");
+    for (int r = 0; r < world; ++r) {
+        if (r == c->d.rank) continue;
+        PeerBlob b;
+        std::memcpy(&b, blobs + (size_t)r * FDW_PEER_BLOB_BYTES, sizeof(b));
+        if (b.magic != PEER_MAGIC || b.rank != r || b.world != world)
+            return fail(c, FDW_EINVAL, "peer blob %d is not rank %d's export", r, r);
+        if (b.pid == (int64_t)getpid())
+            return fail(c, FDW_EINVAL, "peer rank %d lives in this process: use fdw_peer_link", r);
+        if ((s = peer_geometry(c, r, b.ld, b.plane, b.nzl, b.origin, b.tsize, b.R))) return s;
+        void* p = nullptr;
+        CU(cudaIpcOpenMemHandle(&p, b.sync, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_mapped.push_back(p);
+        c->peer_sync[r] = static_cast<fdw::PeerSync*>(p);
+        const int side = r == c->d.rank - 1 ? 0 : r == c->d.rank + 1 ? 1 : -1;
+        if (side >= 0)
+            for (int l = 0; l < 2; ++l) {
+                CU(cudaIpcOpenMemHandle(&p, b.lvl[l], cudaIpcMemLazyEnablePeerAccess));
+                c->ipc_mapped.push_back(p);
+                c->peer_lvl[side][l] = p;
+            }
+    }
+    c->peers_ready = true;
+    return FDW_OK;
+}
+
+fdw_status fdw_peer_link(fdw_solver* c, fdw_solver* const* all, int32_t world) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (!c->peer_mode) return fail(c, FDW_EINVAL, "not a peer-transport slab context");
+    if (!all || world != c->d.world) return fail(c, FDW_EINVAL, "need one context per rank (%d)", c->d.world);
+    if (c->peers_ready) return fail(c, FDW_ESTATE, "peers already linked");
+    for (int r = 0; r < world; ++r) {
+        const fdw_solver* o = all[r];
+        if (r == c->d.rank) {
+            if (o != c) return fail(c, FDW_EINVAL, "all[%d] must be this context", r);
+            continue;
+        }
+        if (!o || !o->peer_mode || o->d.rank != r || o->d.world != world)
+            return fail(c, FDW_EINVAL, "all[%d] is not rank %d of this decomposition", r, r);
+        if ((s = peer_geometry(c, r, o->ld, o->plane, o->nzl, o->origin, o->tsize, o->R))) return s;
+        if (o->d.device != c->d.device) {
+            const cudaError_t e = cudaDeviceEnablePeerAccess(o->d.device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return fail(c, FDW_ECUDA, "cudaDeviceEnablePeerAccess(%d): %s", o->d.device, cudaGetErrorString(e));
+            cudaGetLastError();
+        }
+        c->peer_sync[r] = o->psync;
+        const int side = r == c->d.rank - 1 ? 0 : r == c->d.rank + 1 ? 1 : -1;
+        if (side >= 0)
+            for (int l = 0; l < 2; ++l) c->peer_lvl[side][l] = o->lvl[l];
+    }
+    c->peers_ready = true;
+    return FDW_OK;
 }
 
 fdw_status fdw_nccl_unique_id(unsigned char out[128]) {
@@ -1527,9 +1736,28 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
     }
+    if (c->ndim == 3 && d.world > 1) {
+        bool zero_id = true;
+        for (unsigned char b : d.nccl_id) zero_id = zero_id && b == 0;
+        c->peer_mode = zero_id;
+    }
     for (void** p : {&c->lvl[0], &c->lvl[1], &c->c2dt2, &c->eta}) {
-        if (!ck(cudaMallocAsync(p, bytes, c->stream), "cudaMallocAsync(level)")) return bail(FDW_ENOMEM);
+        // peer transport: the levels are mapped by the neighbours (cudaIpc
+        // needs cudaMalloc memory, not the stream-ordered pool)
+        const bool ipc = c->peer_mode && (p == &c->lvl[0] || p == &c->lvl[1]);
+        if (!ck(ipc ? cudaMalloc(p, bytes) : cudaMallocAsync(p, bytes, c->stream), "cudaMalloc(level)"))
+            return bail(FDW_ENOMEM);
         if (!ck(cudaMemsetAsync(*p, 0, bytes, c->stream), "memset")) return bail(FDW_ECUDA);
+    }
+    if (c->peer_mode) {
+        if (d.world > fdw::PEER_MAX_WORLD) {
+            fail(c, FDW_EINVAL, "peer transport supports at most %d ranks", fdw::PEER_MAX_WORLD);
+            return bail(FDW_EINVAL);
+        }
+        if (!ck(cudaMalloc(reinterpret_cast<void**>(&c->psync), sizeof(fdw::PeerSync)), "cudaMalloc(sync)"))
+            return bail(FDW_ENOMEM);
+        if (!ck(cudaMemsetAsync(c->psync, 0, sizeof(fdw::PeerSync), c->stream), "memset")) return bail(FDW_ECUDA);
+        c->peer_sync[d.rank] = c->psync;
     }
     if (!ck(cudaMallocAsync(reinterpret_cast<void**>(&c->ctrl), sizeof(Ctrl), c->stream), "cudaMallocAsync(ctrl)"))
         return bail(FDW_ENOMEM);
@@ -1599,7 +1827,7 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
         if (c->zseg > c->nzl) c->zseg = (int)c->nzl;
     }
 
-    if (c->d.world > 1) {
+    if (c->d.world > 1 && !c->peer_mode) {
         ncclUniqueId id;
         std::memcpy(&id, d.nccl_id, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&c->comm, c->d.world, id, c->d.rank);
@@ -1643,6 +1871,13 @@ fdw_status fdw_destroy(fdw_solver* c) {
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     lap("graphs");
     if (c->comm) ncclCommDestroy(c->comm);
+    for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
+    if (c->peer_mode) {
+        if (c->stream) cudaStreamSynchronize(c->stream);
+        for (void* p : {c->lvl[0], c->lvl[1], (void*)c->psync})
+            if (p) cudaFree(p);
+        c->lvl[0] = c->lvl[1] = nullptr;
+    }
     for (void* p : {c->lvl[0], c->lvl[1], c->c2dt2, c->eta, c->grad[0], c->grad[1], c->grad[2]})
         if (p) cudaFreeAsync(p, c->stream);
     for (void* p : c->vs_fields) cudaFreeAsync(p, c->stream);

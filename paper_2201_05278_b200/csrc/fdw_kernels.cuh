@@ -28,6 +28,7 @@ struct Ctrl {
     unsigned long long row_base;  // seismogram row 0 = this step (set by fdw_record)
     unsigned int abort;           // latched by the health check; every kernel no-ops
     unsigned int kind;            // 0 finite, 1 inf, 2 nan (|first non-finite|)
+    unsigned int peer_err;        // peer transport: a wait for a neighbour timed out
 };
 
 // ---------------------------------------------------------------------------
@@ -136,6 +137,12 @@ struct SweepArgs {
     // middle).  Used to sweep a slab's boundary planes first and exchange them
     // while the interior is swept.
     int seg_mul, seg_add, zseg_total;  // -0 (runtime value for the packed exact products)
+    // peer transport (Z slabs over NVLink peer memory): the TMA sweep also
+    // stores its first / last R planes into the lower / upper neighbour's ghost
+    // planes of the same level, at element (local index + delta); null: none
+    T* peer_lo;
+    T* peer_hi;
+    long long peer_lo_delta, peer_hi_delta;
     const Ctrl* ctrl;
 };
 
@@ -769,6 +776,29 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
 #pragma unroll
         for (int k = 0; k < 2 * R; ++k) qq[k] = qq[k + 1];
     }
+    // peer transport: this column's share of the first / last R planes goes
+    // straight into the neighbour's ghost planes over NVLink (each thread
+    // re-reads its own just-written outputs; outside the plane loop, so the
+    // hot loop's registers are untouched), performed system-wide before the
+    // grid ends
+    const bool plo = a.peer_lo && zs < R, phi = a.peer_hi && ze > nz - R;
+    if ((plo || phi) && xin) {
+        auto copy_plane = [&](T* peer, long long delta, int z) {
+            const T* o = a.out + col0 + (long long)z * plane;
+            T* po = peer + (col0 + (long long)z * plane + delta);
+            if (y0 + V <= ny) {
+                st16(po, *reinterpret_cast<const VT*>(o));
+            } else {
+                for (int e = 0; e < V; ++e)
+                    if (y0 + e < ny) po[e] = o[e];
+            }
+        };
+        if (plo)
+            for (int z = zs; z < min(ze, R); ++z) copy_plane(a.peer_lo, a.peer_lo_delta, z);
+        if (phi)
+            for (int z = max(zs, nz - R); z < ze; ++z) copy_plane(a.peer_hi, a.peer_hi_delta, z);
+    }
+    if (plo || phi) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -1068,6 +1098,145 @@ __global__ void density_grad_kernel(const T* __restrict__ rho, T* __restrict__ g
 }
 
 // ---------------------------------------------------------------------------
+// Peer transport for Z slabs (one process per GPU on one NVLink/NVSwitch box).
+// A rank's first / last R owned planes are the lower / upper neighbour's ghost
+// planes; they are stored straight into the neighbour's level through mapped
+// peer memory (by the sweep epilogue, by the point-source kernel for targets
+// in those planes, or by peer_push), then one thread per rank signals and
+// waits on step-epoch flags (peer_halo_sync).  No NCCL on the data path.
+template <typename T>
+struct PeerMirror {
+    T* lo = nullptr;             // lower neighbour's level (mapped), or null
+    T* hi = nullptr;             // upper neighbour's level (mapped), or null
+    long long lo_delta = 0, hi_delta = 0;  // neighbour element = local element + delta
+    long long lo_end = 0;        // local elements [origin, lo_end) lie in the first R planes
+    long long hi_begin = 0;      // local elements >= hi_begin lie in the last R planes
+    __device__ __forceinline__ void store(long long i, T v) const {
+        if (lo && i < lo_end) lo[i + lo_delta] = v;
+        if (hi && i >= hi_begin) hi[i + hi_delta] = v;
+    }
+};
+
+constexpr int PEER_MAX_WORLD = 8;
+// Per-rank synchronisation block (device memory, IPC-exported).  Flags are
+// written by the other ranks with st.release.sys and read with ld.acquire.sys.
+struct PeerSync {
+    unsigned long long halo_flag[PEER_MAX_WORLD];    // halo epoch last signalled by rank s
+    unsigned long long health_flag[PEER_MAX_WORLD];  // health epoch last signalled by rank s
+    unsigned long long in_idx[2][PEER_MAX_WORLD];    // health inbox (epoch parity, source rank)
+    unsigned long long in_max[2][PEER_MAX_WORLD];
+    unsigned int in_kind[2][PEER_MAX_WORLD];
+    unsigned long long halo_epoch;                   // this rank's own counters
+    unsigned long long health_epoch;
+};
+
+struct PeerArgs {
+    PeerSync* self;
+    PeerSync* peer[PEER_MAX_WORLD];  // mapped sync blocks of every rank (peer[rank] = self)
+    int rank, world;
+    Ctrl* ctrl;
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// Spins (one thread) until *flag >= want; after ~20 s latches peer_err + abort
+// instead of hanging the device.
+__device__ bool peer_wait_flag(const unsigned long long* flag, unsigned long long want, Ctrl* ctrl) {
+    const unsigned long long t0 = global_ns();
+    unsigned int ns = 32;
+    while (ld_acquire_sys(flag) < want) {
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
+        if (global_ns() - t0 > 20000000000ull) {
+            ctrl->peer_err = 1u;
+            ctrl->abort = 1u;
+            return false;
+        }
+    }
+    return true;
+}
+
+// After a step's writes into the neighbours' ghost planes: signal them, then
+// wait until both neighbours have signalled the same epoch (their writes into
+// this rank's ghost planes are visible, and they are done reading the level
+// this rank writes next).  Runs whether or not the step was aborted, so the
+// epochs of all ranks stay in step.
+__global__ void peer_halo_sync(PeerArgs p) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const unsigned long long e = p.self->halo_epoch + 1;
+    p.self->halo_epoch = e;
+    __threadfence_system();
+    if (p.rank > 0) st_release_sys(&p.peer[p.rank - 1]->halo_flag[p.rank], e);
+    if (p.rank < p.world - 1) st_release_sys(&p.peer[p.rank + 1]->halo_flag[p.rank], e);
+    if (p.rank > 0 && !peer_wait_flag(&p.self->halo_flag[p.rank - 1], e, p.ctrl)) return;
+    if (p.rank < p.world - 1) peer_wait_flag(&p.self->halo_flag[p.rank + 1], e, p.ctrl);
+}
+
+// Health reduction across ranks (replaces the ncclAllReduce min/max calls):
+// every rank stores its (first non-finite index, max |u| bits, kind) into each
+// other rank's inbox slot, signals, waits for all, then reduces locally.
+__global__ void peer_allreduce_health(PeerArgs p) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const unsigned long long e = p.self->health_epoch + 1;
+    p.self->health_epoch = e;
+    const int slot = (int)(e & 1);
+    const unsigned long long idx = p.ctrl->bad_idx, mx = p.ctrl->max_bits;
+    const unsigned int kind = p.ctrl->kind;
+    for (int s = 0; s < p.world; ++s) {
+        if (s == p.rank) continue;
+        PeerSync* d = p.peer[s];
+        d->in_idx[slot][p.rank] = idx;
+        d->in_max[slot][p.rank] = mx;
+        d->in_kind[slot][p.rank] = kind;
+    }
+    __threadfence_system();
+    for (int s = 0; s < p.world; ++s)
+        if (s != p.rank) st_release_sys(&p.peer[s]->health_flag[p.rank], e);
+    unsigned long long r_idx = idx, r_max = mx;
+    unsigned int r_kind = kind;
+    for (int s = 0; s < p.world; ++s) {
+        if (s == p.rank) continue;
+        if (!peer_wait_flag(&p.self->health_flag[s], e, p.ctrl)) return;
+        r_idx = min(r_idx, p.self->in_idx[slot][s]);
+        r_max = max(r_max, p.self->in_max[slot][s]);
+        r_kind = max(r_kind, p.self->in_kind[slot][s]);
+    }
+    p.ctrl->bad_idx = r_idx;
+    p.ctrl->max_bits = r_max;
+    p.ctrl->kind = r_kind;
+}
+
+// Copies this rank's first / last R owned planes (full padded planes,
+// contiguous) into the neighbours' ghost planes: used where the producing
+// kernel did not store them itself (refresh_boundary, uploads, stored-ghost
+// and non-TMA sweeps, volume sources).  16-byte vectors.
+template <typename T>
+__global__ void peer_push(const T* __restrict__ lvl, T* lo, T* hi, long long lo_src, long long lo_delta,
+                          long long hi_src, long long hi_delta, long long n) {
+    using VT = Vec<T, 16 / sizeof(T)>;
+    constexpr int V = 16 / sizeof(T);
+    const long long nv = n / V;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < nv;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long o = t * V;
+        if (lo) *reinterpret_cast<VT*>(lo + lo_src + o + lo_delta) = *reinterpret_cast<const VT*>(lvl + lo_src + o);
+        if (hi) *reinterpret_cast<VT*>(hi + hi_src + o + hi_delta) = *reinterpret_cast<const VT*>(lvl + hi_src + o);
+    }
+    __threadfence_system();
+}
+
+// ---------------------------------------------------------------------------
 // inject, kernel.hpp:429-438.  One thread per distinct target index; its
 // entries are applied in the reference's (point, entry) order.
 template <typename T, bool EXACT>
@@ -1075,7 +1244,8 @@ __global__ void inject_kernel(T* out, const T* __restrict__ c2dt2, const T* __re
                               double dt, const long long* __restrict__ tgt,
                               const unsigned int* __restrict__ ent_off,
                               const double* __restrict__ ent_w, const double* __restrict__ wavelet,
-                              unsigned long long n_wavelet, int n_tgt, int k, const Ctrl* ctrl) {
+                              unsigned long long n_wavelet, int n_tgt, int k, const Ctrl* ctrl,
+                              PeerMirror<T> pm) {
     using A = Ar<T, true>;  // the reference's scalar order; never contracted
     if (ctrl->abort) return;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1092,6 +1262,7 @@ __global__ void inject_kernel(T* out, const T* __restrict__ c2dt2, const T* __re
     for (unsigned int q = ent_off[t]; q < ent_off[t + 1]; ++q)
         val = A::add(val, A::mul(A::mul(c2, static_cast<T>(__dmul_rn(ent_w[q], amp))), iop));
     out[i] = val;
+    pm.store(i, val);
 }
 
 // Dense modulated sources, kernel.hpp:439-452: after the point sources, for

@@ -1,9 +1,11 @@
 """Multi-GPU host plumbing for the Z-slab decomposition (one process per GPU).
 
-The library owns the data path (NCCL send/recv of R halo planes per internal
-face inside the step graph, fdw_api.cu launch_halo); this module only does the
-control-plane work around it with torch.distributed:
-  * broadcast the NCCL unique id from rank 0,
+The library owns the data path: with the peer transport (default) the sweep
+stores the R halo planes straight into the neighbours' levels over NVLink peer
+memory; with the NCCL transport they are exchanged by send/recv inside the step
+graph (fdw_api.cu launch_halo).  This module only does the control-plane work
+around it with torch.distributed:
+  * all-gather the peer IPC blobs (link_peers) or broadcast the NCCL unique id,
   * build each rank's slab workload (configs.build_workload(rank, world)),
   * reduce per-rank partial seismograms in rank order (double) and cast to T,
   * gather halo-stripped slabs for checking.
@@ -28,6 +30,16 @@ def nccl_unique_id(group=None) -> bytes:
     obj = [bytes(buf)]
     dist.broadcast_object_list(obj, src=0, group=group)
     return obj[0]
+
+
+def link_peers(solver, group=None) -> None:
+    """Peer transport (a slab Solver created with nccl_id None): all-gather
+    every rank's IPC export blob and map the neighbours' levels and all sync
+    blocks (fdw_peer_import).  Collective over `group`."""
+    import torch.distributed as dist
+    blobs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(blobs, solver.peer_export(), group=group)
+    solver.peer_import(blobs)
 
 
 def slab_range(n_ext: int, world: int, rank: int) -> tuple:

@@ -432,6 +432,24 @@ class Solver:
                 "variant": var.value & 0xFF, "z_segments": (var.value >> 8) & 0xFF,
                 "ctas_per_sm": var.value >> 16}
 
+    # -- peer transport (Z slabs over NVLink peer memory, no NCCL) --
+    def peer_export(self) -> bytes:
+        """IPC handles of this rank's levels and sync block (fdw_peer_export)."""
+        buf = (C.c_ubyte * _lib.FDW_PEER_BLOB_BYTES)()
+        _check(self._ctx, _lib.lib().fdw_peer_export(self._ctx, C.byref(buf)), "fdw_peer_export")
+        return bytes(buf)
+
+    def peer_import(self, blobs) -> None:
+        """Every rank's peer_export() blob in rank order (one process per GPU)."""
+        data = b"".join(bytes(b) for b in blobs)
+        buf = (C.c_ubyte * len(data)).from_buffer_copy(data)
+        _check(self._ctx, _lib.lib().fdw_peer_import(self._ctx, C.byref(buf), len(blobs)), "fdw_peer_import")
+
+    def peer_link(self, solvers) -> None:
+        """All ranks' Solvers driven from this process (one thread per rank)."""
+        arr = (C.c_void_p * len(solvers))(*[s._ctx.value for s in solvers])
+        _check(self._ctx, _lib.lib().fdw_peer_link(self._ctx, arr, len(solvers)), "fdw_peer_link")
+
     def set_stream(self, stream_ptr: int):
         _check(self._ctx, _lib.lib().fdw_set_stream(self._ctx, C.c_void_p(stream_ptr)), "fdw_set_stream")
 

@@ -1,0 +1,77 @@
+"""Peer transport (Z slabs, no NCCL) on one GPU: world 2 and 3 slabs driven
+from one process, one host thread per rank (fdw_peer_link).  Each step's TMA
+sweep stores its first / last R planes straight into the neighbours' levels,
+the point-source kernel mirrors targets in those planes, and one thread per
+rank signals / waits on step epochs in the sync blocks.  No kernel waits on a
+kernel of the same stream or on a grid that could be starved: the only waiters
+are 1-thread sync kernels, the sweeps never spin.
+
+The assembled wavefield must be bit-identical to the single-domain oracle; the
+seismogram equals the oracle's up to the split of each receiver's double sum at
+slab faces (as in test_slabs_gloo.py)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+CHILD = r'''
+import os, sys, threading
+root = os.path.dirname({here!r})
+for p in (root, os.path.join(root, "oracle"), {here!r}):
+    sys.path.insert(0, p)
+import numpy as np
+from helpers import D, N, X, gpu_solver, oracle_solver, same, small_config
+from paper_2201_05278_b200.configs import build_workload
+h = 20.0
+shape = (41, 27, 25)   # extended Z = 51 planes: slabs 26/25 (world 2), 17/17/17 (world 3)
+cases = [(2, [(h * 20.5, h * 13.5, h * 12.5)]),                        # taps across the 2-slab face
+         (3, [(h * 11.5, h * 13.5, h * 12.5), (h * 28.5, h * 9.5, h * 10.5)])]
+for world, src in cases:
+    cfg = small_config(ndim=3, order=8, shape=shape, bc=[[N, D], [D, X], [D, N]], src=src, n_rec=9)
+    for dt in (np.float32, np.float64):
+        ws = [build_workload(cfg, dt, rank=r, world=world) for r in range(world)]
+        ss = [gpu_solver(w, slab=(*w.slab, None), z_segments=3) for w in ws]
+        for s, w in zip(ss, ws):
+            assert s.layout()["variant"] == 3
+            s.set_sources(w.sources, w.wavelet)
+            s.set_receivers(w.receivers)
+        for s in ss:
+            s.peer_link(ss)
+        out = [None] * world
+        err = []
+        def run(r):
+            try:
+                out[r] = ss[r].forward()
+            except Exception as e:  # surfaced below
+                err.append(repr(e))
+        th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in th: t.start()
+        for t in th: t.join(120)
+        assert not err, err
+        full = np.concatenate([o.snapshots[-1] for o in out], axis=0)
+        seis = sum(s.seismogram_f64() for s in ss)
+        w = build_workload(cfg, dt)
+        o = oracle_solver(w)
+        o.set_sources(w.sources, w.wavelet)
+        o.set_receivers(w.receivers)
+        ref = o.forward()
+        assert np.abs(ref["final"]).max() > 0
+        assert same(full, ref["final"]), (world, dt, float(np.abs(full - ref["final"]).max()))
+        want = np.asarray(ref["seismogram"], np.float64).reshape(seis.shape)
+        tol = 1e-6 if dt == np.float32 else 1e-12
+        assert np.allclose(seis, want, rtol=tol, atol=tol * np.abs(want).max()), (world, dt)
+        for s in ss: s.close()
+        print("peer ok", world, np.dtype(dt).name, flush=True)
+print("peer all ok")
+'''
+
+
+def test_peer_transport_slabs_bit_exact_on_one_gpu():
+    r = subprocess.run([sys.executable, "-c", CHILD.format(here=HERE)], capture_output=True, text=True,
+                       timeout=900, cwd=os.path.dirname(HERE))
+    assert r.returncode == 0 and "peer all ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("peer ok") == 4, r.stdout
