@@ -188,13 +188,6 @@ struct fdw_solver {
     // peer transport (Z slabs, world > 1 with an all-zero nccl_id): halo
     // planes stored straight into the neighbours' levels over NVLink, step
     // epochs and the health reduction through per-rank sync blocks
-    // point sources fused into the TMA sweep: targets regrouped per work
-    // item (Z segment, X tile, Y tile) for the segment count fi_S
-    int fi_S = -1;
-    long long* d_fi_tgt = nullptr;
-    unsigned int* d_fi_eoff = nullptr;
-    double* d_fi_w = nullptr;
-    int* d_fi_item = nullptr;
     bool peer_mode = false;
     bool peers_ready = false;
     fdw::PeerSync* psync = nullptr;                        // own sync block (cudaMalloc, IPC-exportable)
@@ -479,20 +472,10 @@ const void* tma_kernel(int R, bool ex, int minb) {
 }
 
 template <typename T, bool EX>
-bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst, int gz = 0, cudaStream_t st = nullptr,
-                int inj_k = -1) {
+bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst, int gz = 0, cudaStream_t st = nullptr) {
     using S4 = fdw::TmaShape<T, 4, TMA_BX>;
     if (!st) st = c->stream;
     SweepArgs<T> a = a0;
-    if (inj_k >= 0 && c->fi_S == c->zseg && c->n_tgt > 0) {  // point sources fused (fused_inject)
-        a.fi_tgt = c->d_fi_tgt;
-        a.fi_eoff = c->d_fi_eoff;
-        a.fi_w = c->d_fi_w;
-        a.fi_item = c->d_fi_item;
-        a.wavelet = c->d_wavelet;
-        a.n_wavelet = c->n_wavelet;
-        a.inj_k = inj_k;
-    }
     if (c->peer_mode && c->peers_ready) {  // fused halo stores (see enqueue_step)
         a.peer_lo = static_cast<T*>(c->peer_lvl[0][dst]);
         a.peer_hi = static_cast<T*>(c->peer_lvl[1][dst]);
@@ -688,7 +671,7 @@ int zmarch_occupancy(int R, bool exact) {
 }
 
 template <typename T>
-fdw_status launch_sweep_t(fdw_solver* c, int src, int dst, bool virt, int inj_k) {
+fdw_status launch_sweep_t(fdw_solver* c, int src, int dst, bool virt) {
     const SweepArgs<T> a = sweep_args<T>(c, src, dst);
     const bool ex = c->d.math == FDW_MATH_EXACT;
     if (c->vd && !(c->variant == FDW_KERNEL_TMA && virt)) {
@@ -702,8 +685,7 @@ fdw_status launch_sweep_t(fdw_solver* c, int src, int dst, bool virt, int inj_k)
         const bool ok = ex ? launch_zmarch<T, true>(c, a) : launch_zmarch<T, false>(c, a);
         if (!ok) return fail(c, FDW_EINVAL, "zmarch kernel not built for radius %d", c->R);
     } else if (c->variant == FDW_KERNEL_TMA) {
-        const bool ok = ex ? launch_tma<T, true>(c, a, src, dst, 0, nullptr, inj_k)
-                           : launch_tma<T, false>(c, a, src, dst, 0, nullptr, inj_k);
+        const bool ok = ex ? launch_tma<T, true>(c, a, src, dst) : launch_tma<T, false>(c, a, src, dst);
         if (!ok) return fail(c, FDW_EINVAL, "TMA kernel not built for radius %d", c->R);
     } else if (c->variant == FDW_KERNEL_ZMARCH) {
         const bool ok = ex ? launch_zmarch<T, true>(c, a) : launch_zmarch<T, false>(c, a);
@@ -718,60 +700,8 @@ fdw_status launch_sweep_t(fdw_solver* c, int src, int dst, bool virt, int inj_k)
     return FDW_OK;
 }
 
-fdw_status launch_sweep(fdw_solver* c, int src, int dst, bool virt, int inj_k = -1) {
-    return c->tsize == 4 ? launch_sweep_t<float>(c, src, dst, virt, inj_k)
-                         : launch_sweep_t<double>(c, src, dst, virt, inj_k);
-}
-
-template <typename P>
-fdw_status dev_upload(fdw_solver* c, P** dst, const std::vector<P>& v);
-
-// The point sources of a virtual-ghost TMA step ride in the sweep (after each
-// work item's column segment) instead of a separate inject launch.
-bool fused_inject(const fdw_solver* c, bool virt) {
-    static const bool off = std::getenv("FDW_NO_FUSED_INJECT") != nullptr;
-    if (off || c->variant != FDW_KERNEL_TMA || !virt || c->ndim != 3 || c->n_tgt == 0) return false;
-    return c->fi_S == c->zseg;
-}
-
-// Groups the merged targets by the TMA work item that writes them (per-target
-// entry order untouched); rebuilt when the Z-segment count changes.
-fdw_status ensure_fused_inject(fdw_solver* c) {
-    if (c->variant != FDW_KERNEL_TMA || c->ndim != 3 || c->fi_S == c->zseg) return FDW_OK;
-    const int S = c->zseg;
-    const long long tyw = 64 / (c->tsize / 4), bxr = TMA_BX;
-    const long long ty_n = (c->nyl + tyw - 1) / tyw, tx_n = (c->nxl + bxr - 1) / bxr;
-    const long long n_items = ty_n * tx_n * S;
-    std::vector<std::vector<int>> by_item((size_t)n_items);
-    for (size_t t = 0; t < c->h_tgt.size(); ++t) {
-        const long long rem = c->h_tgt[t] - c->origin;
-        const long long z = rem / c->plane, r2 = rem % c->plane, x = r2 / c->ld, y = r2 % c->ld;
-        int seg = 0;
-        while (seg + 1 < S && (long long)c->nzl * (seg + 1) / S <= z) ++seg;
-        const long long it = ((long long)seg * tx_n + x / bxr) * ty_n + y / tyw;
-        if (z < 0 || z >= c->nzl || x < 0 || x >= c->nxl || y < 0 || y >= c->nyl || it < 0 || it >= n_items)
-            return fail(c, FDW_EINVAL, "source target outside the extended slab");
-        by_item[(size_t)it].push_back((int)t);
-    }
-    std::vector<long long> tg;
-    std::vector<unsigned int> eo(1, 0);
-    std::vector<double> ew;
-    std::vector<int> io(1, 0);
-    for (auto& v : by_item) {
-        for (int t : v) {
-            tg.push_back(c->h_tgt[t]);
-            ew.insert(ew.end(), c->h_tw[t].begin(), c->h_tw[t].end());
-            eo.push_back((unsigned int)ew.size());
-        }
-        io.push_back((int)tg.size());
-    }
-    fdw_status s;
-    if ((s = dev_upload(c, &c->d_fi_tgt, tg))) return s;
-    if ((s = dev_upload(c, &c->d_fi_eoff, eo))) return s;
-    if ((s = dev_upload(c, &c->d_fi_w, ew))) return s;
-    if ((s = dev_upload(c, &c->d_fi_item, io))) return s;
-    c->fi_S = S;
-    return FDW_OK;
+fdw_status launch_sweep(fdw_solver* c, int src, int dst, bool virt) {
+    return c->tsize == 4 ? launch_sweep_t<float>(c, src, dst, virt) : launch_sweep_t<double>(c, src, dst, virt);
 }
 
 template <typename T>
@@ -1181,15 +1111,8 @@ fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
         s = c->tsize == 4 ? enqueue_split_sweep_t<float>(c, k, src, dst) : enqueue_split_sweep_t<double>(c, k, src, dst);
         if (s) return s;
     } else {
-        const bool fi = fused_inject(c, virt);
-        { Mark m(c, 0); if ((s = launch_sweep(c, src, dst, virt, fi ? k : -1))) return s; }
-        if (fi) {  // point sources already applied by the sweep; volume sources follow
-            Mark m(c, 1);
-            if ((s = c->tsize == 4 ? launch_volume_t<float>(c, dst, k) : launch_volume_t<double>(c, dst, k))) return s;
-        } else {
-            Mark m(c, 1);
-            if ((s = launch_inject(c, dst, k))) return s;
-        }
+        { Mark m(c, 0); if ((s = launch_sweep(c, src, dst, virt))) return s; }
+        { Mark m(c, 1); if ((s = launch_inject(c, dst, k))) return s; }
         // swap: dst is now the current level
         if (!virt) { Mark m(c, 2); if ((s = launch_faces(c, dst))) return s; }
         if (c->d.world > 1 && c->peer_mode) {
@@ -1254,10 +1177,6 @@ fdw_status enqueue_chunk(fdw_solver* c, unsigned long long L, int cur0, bool che
 fdw_status run_chunk(fdw_solver* c, unsigned long long L, bool check, bool record) {
     if (split_step(c, true)) {  // (uploads; never inside a capture)
         fdw_status s = ensure_target_split(c);
-        if (s) return s;
-    }
-    if (c->n_tgt > 0) {  // (uploads; never inside a capture)
-        fdw_status s = ensure_fused_inject(c);
         if (s) return s;
     }
     const int cur0 = c->cur;
@@ -1964,8 +1883,6 @@ fdw_status fdw_destroy(fdw_solver* c) {
     for (void* p : c->vs_fields) cudaFreeAsync(p, c->stream);
     for (void* p : {c->d_vs_ptrs, c->d_vs_amp, (void*)c->d_vs_len})
         if (p) cudaFreeAsync(p, c->stream);
-    for (void* p : {(void*)c->d_fi_tgt, (void*)c->d_fi_eoff, (void*)c->d_fi_w, (void*)c->d_fi_item})
-        if (p) cudaFreeAsync(p, c->stream);
     for (void* p : {(void*)c->d_ezr, (void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off, (void*)c->d_ent_w, (void*)c->d_wavelet,
                     (void*)c->d_rec_idx, (void*)c->d_rec_off, (void*)c->d_rec_w, (void*)c->d_seis, (void*)c->d_tmap})
         if (p) cudaFreeAsync(p, c->stream);
@@ -2180,7 +2097,6 @@ fdw_status fdw_set_sources(fdw_solver* c, uint64_t n_points, const uint64_t* off
     c->h_tw = ws;
     c->split_S = -1;
     c->n_tgt_a = 0;
-    c->fi_S = -1;
     if ((s = dev_upload(c, &c->d_tgt, tgt))) return s;
     if ((s = dev_upload(c, &c->d_ent_off, eo))) return s;
     if ((s = dev_upload(c, &c->d_ent_w, ew))) return s;

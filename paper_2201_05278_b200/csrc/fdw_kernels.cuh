@@ -143,17 +143,6 @@ struct SweepArgs {
     T* peer_lo;
     T* peer_hi;
     long long peer_lo_delta, peer_hi_delta;
-    // TMA sweep with the point sources fused (inject, kernel.hpp:429-438): the
-    // targets of work item (Z segment, X tile, Y tile) are fi_tgt[fi_item[it]
-    // .. fi_item[it+1]), entries CSR in fi_eoff / fi_w; step = ctrl->step +
-    // inj_k; null fi_item: no fused injection
-    const long long* fi_tgt;
-    const unsigned int* fi_eoff;
-    const double* fi_w;
-    const int* fi_item;
-    const double* wavelet;
-    unsigned long long n_wavelet;
-    int inj_k;
     const Ctrl* ctrl;
 };
 
@@ -787,50 +776,21 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
 #pragma unroll
         for (int k = 0; k < 2 * R; ++k) qq[k] = qq[k + 1];
     }
-    // Point sources of this work item (inject, kernel.hpp:429-438), after the
-    // whole column segment is written: one thread per target, entries in the
-    // reference's (point, entry) order; same arithmetic as inject_kernel.
-    // Outside the plane loop, so the hot loop's registers are untouched.
-    if (a.fi_item) {
-        const int item = (seg * (int)gridDim.y + (int)blockIdx.y) * (int)gridDim.x + (int)blockIdx.x;
-        const int t0 = a.fi_item[item], t1 = a.fi_item[item + 1];
-        const unsigned long long n = a.ctrl->step + (unsigned long long)a.inj_k;
-        if (t0 < t1 && n < a.n_wavelet) {  // uniform over the CTA
-            using AX = Ar<T, true>;
-            __syncthreads();  // every output of this CTA is stored
-            const double amp = a.wavelet[n];
-            for (int t = t0 + tid; t < t1; t += THREADS) {
-                const long long i = a.fi_tgt[t];
-                const T c2 = a.c2dt2[i];
-                const T e = a.eta[i];
-                T om, iop = T(1);
-                if (e != T(0)) damping_factors(e, a.dt, om, iop);
-                T val = __ldcg(a.out + i);
-                for (unsigned int q = a.fi_eoff[t]; q < a.fi_eoff[t + 1]; ++q)
-                    val = AX::add(val, AX::mul(AX::mul(c2, static_cast<T>(__dmul_rn(a.fi_w[q], amp))), iop));
-                a.out[i] = val;
-            }
-            __syncthreads();  // injected values visible to the peer copy below
-        }
-    }
     // peer transport: this column's share of the first / last R planes goes
     // straight into the neighbour's ghost planes over NVLink (each thread
-    // re-reads the just-written outputs from L2; outside the plane loop, so
-    // the hot loop's registers are untouched), performed system-wide before
-    // the grid ends
+    // re-reads its own just-written outputs; outside the plane loop, so the
+    // hot loop's registers are untouched), performed system-wide before the
+    // grid ends
     const bool plo = a.peer_lo && zs < R, phi = a.peer_hi && ze > nz - R;
     if ((plo || phi) && xin) {
         auto copy_plane = [&](T* peer, long long delta, int z) {
             const T* o = a.out + col0 + (long long)z * plane;
             T* po = peer + (col0 + (long long)z * plane + delta);
             if (y0 + V <= ny) {
-                VT v;
-#pragma unroll
-                for (int e = 0; e < V; ++e) v.e[e] = __ldcg(o + e);
-                st16(po, v);
+                st16(po, *reinterpret_cast<const VT*>(o));
             } else {
                 for (int e = 0; e < V; ++e)
-                    if (y0 + e < ny) po[e] = __ldcg(o + e);
+                    if (y0 + e < ny) po[e] = o[e];
             }
         };
         if (plo)
