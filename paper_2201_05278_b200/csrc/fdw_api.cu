@@ -609,8 +609,23 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+// L2 promotion of the TMA loads: FDW_TMA_PROMO_U (u tiles, default 64 B) /
+// FDW_TMA_PROMO_P (prev, c2dt2, eta tiles, default 256 B) = 0, 64, 128 or 256.
+// The u tile rows start 16 B before a 128-B line (the Y halo); promoting those
+// slivers to 256 B fetched neighbour data that missed L2 later: C4 sweep DRAM
+// reads 2.155 -> 2.100 GB with 64 B (profiles/r01/power_cap.txt).
+CUtensorMapL2promotion promo_env(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    const int v = e ? std::atoi(e) : dflt;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+         : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                    : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 // 3D map over one pitched level: dims (ld, rows_alloc, planes), box (bw, bh, 1)
-bool make_map(const fdw_solver* c, CUtensorMap* m, void* base, int bw, int bh) {
+bool make_map(const fdw_solver* c, CUtensorMap* m, void* base, int bw, int bh,
+              CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
     auto fn = encode_fn();
     if (!fn) return false;
     const cuuint64_t dims[3] = {(cuuint64_t)c->ld, (cuuint64_t)c->rows_alloc, (cuuint64_t)(c->Lz + 1)};
@@ -619,7 +634,7 @@ bool make_map(const fdw_solver* c, CUtensorMap* m, void* base, int bw, int bh) {
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = fn(m, c->tsize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
                           base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -642,12 +657,13 @@ bool make_maps_t(fdw_solver* c) {
         default: return false;
     }
     bool ok = true;
+    const CUtensorMapL2promotion pu = promo_env("FDW_TMA_PROMO_U", 64), pp = promo_env("FDW_TMA_PROMO_P", 256);
     for (int l = 0; l < 2; ++l) {
-        ok &= make_map(c, &c->tm_u[l], c->lvl[l], uw, uh);
-        ok &= make_map(c, &c->tm_p[l], c->lvl[l], pw, ph);
+        ok &= make_map(c, &c->tm_u[l], c->lvl[l], uw, uh, pu);
+        ok &= make_map(c, &c->tm_p[l], c->lvl[l], pw, ph, pp);
     }
-    ok &= make_map(c, &c->tm_c, c->c2dt2, pw, ph);
-    ok &= make_map(c, &c->tm_e, c->eta, pw, ph);
+    ok &= make_map(c, &c->tm_c, c->c2dt2, pw, ph, pp);
+    ok &= make_map(c, &c->tm_e, c->eta, pw, ph, pp);
     return ok;
 }
 
