@@ -185,6 +185,21 @@ struct fdw_solver {
     size_t snap_bytes = 0;
     int snap_next = 0;
     int fused_grid = 0;          // FUSED2D: co-resident blocks of the cooperative kernel
+    // FUSED2D, shared-memory resident kernel (constant density): block rows,
+    // blocks per grid row, blocks, dynamic smem; per-block source / tap lists
+    bool res2d = false;
+    int res_BZ = 0, res_xb = 0, res_nb = 0;
+    size_t res_smem = 0;
+    int* d_blk_toff = nullptr;
+    int* d_blk_tgt = nullptr;
+    int* d_blk_tpos = nullptr;
+    int* d_blk_roff = nullptr;
+    int* d_blk_rpack = nullptr;
+    int* d_tap_ix = nullptr;
+    int res_tapcap = 0;
+    size_t res_smem_base = 0;
+    void* d_tapbuf = nullptr;
+    int n_ent = 0;
     // peer transport (Z slabs, world > 1 with an all-zero nccl_id): halo
     // planes stored straight into the neighbours' levels over NVLink, step
     // epochs and the health reduction through per-rank sync blocks
@@ -536,8 +551,132 @@ const void* fused2d_kernel(int R, bool ex, bool vd = false) {
     return ex ? fused2d_fn<T, true>(R) : fused2d_fn<T, false>(R);
 }
 
+template <typename T, bool EX>
+const void* res2d_fn(int R) {
+#define RF(RR) \
+    if (R == RR) return (const void*)fdw::step2d_resident<T, RR, EX>;
+    RF(1) RF(2) RF(3) RF(4) RF(5) RF(6) RF(7) RF(8) RF(9) RF(10)
+#undef RF
+    return nullptr;
+}
+
+template <typename T>
+const void* res2d_kernel(int R, bool ex) {
+    return ex ? res2d_fn<T, true>(R) : res2d_fn<T, false>(R);
+}
+
+template <typename T>
+fdw_status launch_res2d_t(fdw_solver* c, int L, int cur0, bool record) {
+    fdw::Res2DArgs<T> a{};
+    a.lvl[0] = static_cast<T*>(c->lvl[0]);
+    a.lvl[1] = static_cast<T*>(c->lvl[1]);
+    a.c2dt2 = static_cast<const T*>(c->c2dt2);
+    a.eta = static_cast<const T*>(c->eta);
+    for (int j = 0; j <= c->R; ++j) a.v[j] = static_cast<T>(c->d.coeffs[j]);
+    for (int k = 0; k < 2; ++k) a.ih[k] = static_cast<T>(1.0 / (c->d.spacing[k] * c->d.spacing[k]));
+    a.dt = c->d.dt;
+    a.ld = c->ld;
+    a.origin = c->origin;
+    a.nz = (int)c->nzl;
+    a.nx = (int)c->nxl;
+    for (int ax = 0; ax < 2; ++ax)
+        for (int sd = 0; sd < 2; ++sd) {
+            const int bc = c->d.bc[ax][sd];
+            a.gf[ax][sd] = bc == FDW_BC_NULL_DIRICHLET ? -1 : bc == FDW_BC_NULL_NEUMANN ? 1 : 0;
+        }
+    a.BZ = c->res_BZ;
+    a.xb = c->res_xb;
+    a.blk_toff = c->d_blk_toff;
+    a.blk_tgt = c->d_blk_tgt;
+    a.blk_tpos = c->d_blk_tpos;
+    a.ent_off = c->d_ent_off;
+    a.ent_w = c->d_ent_w;
+    a.wavelet = c->d_wavelet;
+    a.n_wavelet = c->n_wavelet;
+    a.blk_roff = c->d_blk_roff;
+    a.blk_rpack = c->d_blk_rpack;
+    a.tap_ix = c->d_tap_ix;
+    a.tapcap = c->res_tapcap;
+    a.tapbuf = static_cast<T*>(c->d_tapbuf);
+    a.n_ent = c->n_ent;
+    a.roff = c->d_rec_off;
+    a.rw = c->d_rec_w;
+    a.seis = c->d_seis;
+    a.n_rec = c->d_seis ? c->n_rec : 0;
+    a.n_rows = c->seis_rows;
+    a.ctrl = c->ctrl;
+    int rec = record && c->d_seis && c->d_tapbuf ? 1 : 0;
+    void* args[] = {&a, &L, &cur0, &rec};
+    const void* f = res2d_kernel<T>(c->R, c->d.math == FDW_MATH_EXACT);
+    if (!f) return fail(c, FDW_EINVAL, "resident 2D kernel not built for this configuration");
+    CU(cudaLaunchCooperativeKernel(f, dim3((unsigned)c->res_nb), dim3(256), args, c->res_smem, c->stream));
+    if (c->capturing)
+        ++c->capture_kernels;
+    else
+        ++c->launches;
+    return FDW_OK;
+}
+
+// Block decomposition of the resident 2D kernel: the largest co-resident
+// occupancy whose blocks fit shared memory and leave every block at least
+// 2R rows and 2*HY columns (mirror sources and strips stay inside a block).
+template <typename T>
+bool res2d_configure(fdw_solver* c) {
+    if (std::getenv("FDW_NO_RESIDENT2D")) return false;
+    const int V = 16 / (int)sizeof(T), TX = 16 * V, R = c->R, HY = ((R + V - 1) / V) * V, UW = TX + 2 * HY;
+    const long long nz = c->nzl, nx = c->nxl;
+    const int xb = (int)((nx + TX - 1) / TX);
+    if (nx - (long long)(xb - 1) * TX < 2 * HY) return false;
+    const void* f = res2d_kernel<T>(R, c->d.math == FDW_MATH_EXACT);
+    if (!f) return false;
+    for (int occ = 3; occ >= 1; --occ) {
+        const long long cap = (long long)occ * c->sm_count;
+        const long long zbn0 = std::min<long long>(nz, cap / xb);
+        if (zbn0 < 1) continue;
+        const int BZ = (int)((nz + zbn0 - 1) / zbn0);
+        const int zbn = (int)((nz + BZ - 1) / BZ);
+        if (BZ < 2 * R || nz - (long long)(zbn - 1) * BZ < 2 * R) continue;
+        const size_t smem =
+            (size_t)(2 * (BZ + 2 * R) * UW + 3 * BZ * TX) * sizeof(T) + 8 * fdw::F2D_CHUNK * sizeof(double);
+        if (smem > 227 * 1024) continue;
+        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        int got = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&got, f, 256, smem) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if ((long long)zbn * xb > (long long)got * c->sm_count) continue;
+        c->res2d = true;
+        c->res_BZ = BZ;
+        c->res_xb = xb;
+        c->res_nb = zbn * xb;
+        c->res_smem = smem;
+        c->res_smem_base = smem;
+        c->occupancy = got;
+        return true;
+    }
+    return false;
+}
+
+// smem offset of extended (z, x) inside its block of the resident 2D kernel
+long long res2d_block_of(const fdw_solver* c, long long z, long long x, int* pos) {
+    const int V = 16 / c->tsize, TX = 16 * V, HY = ((c->R + V - 1) / V) * V, UW = TX + 2 * HY;
+    const long long bz = z / c->res_BZ, bx = x / TX;
+    *pos = (int)((z - bz * c->res_BZ + c->R) * UW + (x - bx * TX + HY));
+    return bz * c->res_xb + bx;
+}
+
+// Per-block point-source list of the resident 2D kernel (merged targets).
+fdw_status res2d_sources(fdw_solver* c);
+// Per-block receiver-tap list of the resident 2D kernel (ghost taps mirrored).
+fdw_status res2d_receivers(fdw_solver* c, const std::vector<long long>& ri);
+
 template <typename T>
 fdw_status launch_fused2d_t(fdw_solver* c, int L, int cur0, bool record, int k0) {
+    if (c->res2d && !c->vd && k0 == 0) return launch_res2d_t<T>(c, L, cur0, record);
     fdw::Fused2DArgs<T> a{};
     a.lvl[0] = static_cast<T*>(c->lvl[0]);
     a.lvl[1] = static_cast<T*>(c->lvl[1]);
@@ -1037,6 +1176,102 @@ fdw_status dev_upload(fdw_solver* c, P** dst, const std::vector<P>& v) {
     const size_t n = std::max<size_t>(v.size(), 1);
     CU(cudaMallocAsync(reinterpret_cast<void**>(dst), n * sizeof(P), c->stream));
     if (!v.empty()) CU(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(P), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status res2d_sources(fdw_solver* c) {
+    const int nb = c->res_nb;
+    std::vector<std::vector<std::pair<int, int>>> per((size_t)nb);
+    for (size_t t = 0; t < c->h_tgt.size(); ++t) {
+        const long long rem = c->h_tgt[t] - c->origin;
+        const long long z = rem / c->ld, x = rem % c->ld;
+        if (rem < 0 || z >= c->nzl || x >= c->nxl) return fail(c, FDW_EINVAL, "source target outside the grid");
+        int pos = 0;
+        const long long b = res2d_block_of(c, z, x, &pos);
+        per[(size_t)b].push_back({(int)t, pos});
+    }
+    std::vector<int> off(1, 0), tg, ps;
+    for (auto& v : per) {
+        for (auto& e : v) {
+            tg.push_back(e.first);
+            ps.push_back(e.second);
+        }
+        off.push_back((int)tg.size());
+    }
+    fdw_status s;
+    if ((s = dev_upload(c, &c->d_blk_toff, off))) return s;
+    if ((s = dev_upload(c, &c->d_blk_tgt, tg))) return s;
+    return dev_upload(c, &c->d_blk_tpos, ps);
+}
+
+// Receiver taps as apply_boundary leaves the level (kernel.hpp:67-102): a tap
+// in a ghost cell reads the mirrored extended point times the faces' factors
+// (-1 Dirichlet, +1 Neumann; "none" gives 0), corners both axes.
+fdw_status res2d_receivers(fdw_solver* c, const std::vector<long long>& ri) {
+    const int nb = c->res_nb;
+    const int n = (int)ri.size();
+    std::vector<std::vector<std::tuple<int, int, int>>> per((size_t)nb);  // (entry, smem offset, factor)
+    auto fac = [&](int ax, int side) {
+        const int bc = c->d.bc[ax][side];
+        return bc == FDW_BC_NULL_DIRICHLET ? -1 : bc == FDW_BC_NULL_NEUMANN ? 1 : 0;
+    };
+    for (int e = 0; e < n; ++e) {
+        // offset = origin + z*ld + x with x in [-R, nx+R) and ld > nx + 2R
+        const long long q = ri[(size_t)e] - c->origin + c->R;
+        long long z = q >= 0 ? q / c->ld : -((-q + c->ld - 1) / c->ld);
+        long long x = q - z * c->ld - c->R;
+        int f = 1;
+        if (z < 0) { z = -z; f *= fac(0, 0); }
+        if (z >= c->nzl) { z = 2 * (c->nzl - 1) - z; f *= fac(0, 1); }
+        if (x < 0) { x = -x; f *= fac(1, 0); }
+        if (x >= c->nxl) { x = 2 * (c->nxl - 1) - x; f *= fac(1, 1); }
+        if (z < 0 || z >= c->nzl || x < 0 || x >= c->nxl) return fail(c, FDW_EINVAL, "receiver tap outside the grid");
+        if (f == 0) {
+            per[0].push_back({e, -1, 0});
+            continue;
+        }
+        int pos = 0;
+        const long long b = res2d_block_of(c, z, x, &pos);
+        per[(size_t)b].push_back({e, pos, f});
+    }
+    std::vector<int> off(1, 0), pack, ix((size_t)std::max(n, 1), 0);
+    int most = 0;
+    for (auto& v : per) {
+        for (auto& t : v) {
+            ix[(size_t)std::get<0>(t)] = (int)pack.size();
+            const int pos = std::max(std::get<1>(t), 0);
+            pack.push_back((pos << 2) | (std::get<2>(t) + 1));
+        }
+        most = std::max(most, (int)v.size());
+        off.push_back((int)pack.size());
+    }
+    fdw_status s;
+    if ((s = dev_upload(c, &c->d_blk_roff, off))) return s;
+    if ((s = dev_upload(c, &c->d_blk_rpack, pack))) return s;
+    if ((s = dev_upload(c, &c->d_tap_ix, ix))) return s;
+    // cache each block's tap list in shared memory when the grid still fits
+    c->res_tapcap = 0;
+    c->res_smem = c->res_smem_base;
+    if (most > 0 && most <= 16384) {
+        const size_t smem = c->res_smem_base + (size_t)most * sizeof(int);
+        const void* f = c->tsize == 4 ? res2d_kernel<float>(c->R, c->d.math == FDW_MATH_EXACT)
+                                      : res2d_kernel<double>(c->R, c->d.math == FDW_MATH_EXACT);
+        int got = 0;
+        if (smem <= 227 * 1024 && cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+                                      cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&got, f, 256, smem) == cudaSuccess &&
+            (long long)c->res_nb <= (long long)got * c->sm_count) {
+            c->res_tapcap = most;
+            c->res_smem = smem;
+        }
+        cudaGetLastError();
+    }
+    if (c->d_tapbuf) cudaFreeAsync(c->d_tapbuf, c->stream);
+    c->d_tapbuf = nullptr;
+    c->n_ent = n;
+    CU(cudaMallocAsync(&c->d_tapbuf, (size_t)std::max(1, 2 * n) * c->tsize, c->stream));
+    CU(cudaMemsetAsync(c->d_tapbuf, 0, (size_t)std::max(1, 2 * n) * c->tsize, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     return FDW_OK;
 }
@@ -1802,6 +2037,12 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
         if (!ck(cudaMallocAsync(reinterpret_cast<void**>(&c->d_tmap), n, c->stream), "cudaMallocAsync(tmap)"))
             return bail(FDW_ENOMEM);
         if (!ck(cudaMemsetAsync(c->d_tmap, 0, n, c->stream), "memset(tmap)")) return bail(FDW_ECUDA);
+        if (c->tsize == 4 ? res2d_configure<float>(c) : res2d_configure<double>(c)) {
+            std::vector<long long> none;
+            fdw_status rs = res2d_sources(c);
+            if (!rs) rs = res2d_receivers(c, none);
+            if (rs) return bail(rs);
+        }
     }
     if ((variant == FDW_KERNEL_ZMARCH || variant == FDW_KERNEL_TMA) && (c->ndim != 3 || !zmarch_supported(R)))
         variant = FDW_KERNEL_SIMPLE;
@@ -1898,6 +2139,9 @@ fdw_status fdw_destroy(fdw_solver* c) {
         if (p) cudaFreeAsync(p, c->stream);
     for (void* p : c->vs_fields) cudaFreeAsync(p, c->stream);
     for (void* p : {c->d_vs_ptrs, c->d_vs_amp, (void*)c->d_vs_len})
+        if (p) cudaFreeAsync(p, c->stream);
+    for (void* p : {(void*)c->d_blk_toff, (void*)c->d_blk_tgt, (void*)c->d_blk_tpos, (void*)c->d_blk_roff,
+                    (void*)c->d_blk_rpack, (void*)c->d_tap_ix, c->d_tapbuf})
         if (p) cudaFreeAsync(p, c->stream);
     for (void* p : {(void*)c->d_ezr, (void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off, (void*)c->d_ent_w, (void*)c->d_wavelet,
                     (void*)c->d_rec_idx, (void*)c->d_rec_off, (void*)c->d_rec_w, (void*)c->d_seis, (void*)c->d_tmap})
@@ -2120,6 +2364,7 @@ fdw_status fdw_set_sources(fdw_solver* c, uint64_t n_points, const uint64_t* off
     if ((s = dev_upload(c, &c->d_wavelet, wv))) return s;
     c->n_wavelet = wv.size();
     c->n_tgt = (int)tgt.size();
+    if (c->res2d && (s = res2d_sources(c))) return s;
     if (c->d_tmap) {  // FUSED2D: dense map extended point -> target index + 1
         std::vector<int> tm((size_t)(c->nzl * c->nxl), 0);
         for (size_t t = 0; t < tgt.size(); ++t) {
@@ -2154,6 +2399,7 @@ fdw_status fdw_set_receivers(fdw_solver* c, uint64_t n_points, const uint64_t* o
     if ((s = dev_upload(c, &c->d_rec_idx, ri))) return s;
     if ((s = dev_upload(c, &c->d_rec_off, ro))) return s;
     if ((s = dev_upload(c, &c->d_rec_w, rw))) return s;
+    if (c->res2d && (s = res2d_receivers(c, ri))) return s;
     if (c->d_seis) cudaFreeAsync(c->d_seis, c->stream);
     c->d_seis = nullptr;
     c->n_rec = (int)n_points;

@@ -840,6 +840,15 @@ struct Fused2DArgs {
     T i2h[2];                    // 1/(2h) per axis
 };
 
+__device__ __forceinline__ Vec<float, 4> ldcg16(const float* p) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(p));
+    return Vec<float, 4>{{v.x, v.y, v.z, v.w}};
+}
+__device__ __forceinline__ Vec<double, 2> ldcg16(const double* p) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+    return Vec<double, 2>{{v.x, v.y}};
+}
+
 template <typename T>
 __device__ __forceinline__ T ldcg(const T* p) {
     return __ldcg(p);
@@ -997,6 +1006,388 @@ __global__ void __launch_bounds__(256) step2d_fused(Fused2DArgs<T> a, int L, int
     }
     if (record)
         fused2d_receivers(a, a.lvl[cur0 ^ (L & 1)], base + (unsigned long long)L - row_base, gwarp, nwarps, lane, prod);
+}
+
+// ---------------------------------------------------------------------------
+// 2D, shared-memory resident (FDW_KERNEL_FUSED2D, constant density): one
+// persistent cooperative launch per chunk; every CTA keeps ONE block of the
+// grid -- both levels with a radius-R halo, c2dt2 and the two damping factors
+// -- in shared memory for the whole chunk.  Per step only the block's boundary
+// strips go through global memory (L2): the owner stores them into the
+// level's natural positions, and after the grid barrier each neighbour loads
+// them as its halo; physical faces are mirrored from the block itself
+// (apply_boundary, kernel.hpp:67-102).  Point sources of the block are
+// applied in smem (kernel.hpp:429-438); receiver taps are copied to a tap
+// buffer and summed in entry order after the barrier (acquisition.hpp:
+// 150-161).  At the chunk's end the block (and its face ghosts) goes back to
+// global, so the level arrays hold exactly what the step-by-step kernels
+// leave.  Same arithmetic and association as sweep_2d (kernel.hpp:344-379).
+template <typename T>
+struct Res2DArgs {
+    T* lvl[2];
+    const T* __restrict__ c2dt2;
+    const T* __restrict__ eta;
+    T v[11];
+    T ih[2];
+    double dt;
+    long long ld, origin;
+    int nz, nx;
+    int gf[2][2];        // mirror factor per face: -1 Dirichlet, +1 Neumann, 0 none
+    int BZ, xb;          // block rows; blocks per grid row (block b = zb_idx * xb + xb_idx)
+    // point sources: per-block CSR (targets, smem offset r*UW+c) over the merged targets
+    const int* blk_toff;
+    const int* blk_tgt;
+    const int* blk_tpos;
+    const unsigned* ent_off;
+    const double* ent_w;
+    const double* wavelet;
+    unsigned long long n_wavelet;
+    // receivers: per-block CSR of taps, packed (smem offset << 2 | factor + 1);
+    // tap q of the concatenated lists goes to tapbuf[q]; entry e reads tap_ix[e]
+    const int* blk_roff;
+    const int* blk_rpack;
+    const int* tap_ix;
+    int tapcap;          // taps cached in shared memory per block (0: read the list from global)
+    T* tapbuf;           // [2][n_ent]
+    int n_ent;
+    const unsigned* roff;
+    const double* rw;
+    double* seis;
+    int n_rec;
+    unsigned long long n_rows;
+    Ctrl* ctrl;
+};
+
+template <typename T, int R>
+struct Res2DShape {
+    static constexpr int V = 16 / (int)sizeof(T);
+    static constexpr int TX = 16 * V;                      // block columns
+    static constexpr int HY = ((R + V - 1) / V) * V;       // X halo, whole vectors
+    static constexpr int UW = TX + 2 * HY;                 // smem row pitch of a level
+    static __host__ __device__ constexpr int rows(int BZ) { return BZ + 2 * R; }
+    static __host__ __device__ constexpr size_t smem(int BZ, int tapcap = 0) {
+        return (size_t)(2 * rows(BZ) * UW + 3 * BZ * TX) * sizeof(T) + 8 * F2D_CHUNK * sizeof(double) +
+               (size_t)tapcap * sizeof(int);
+    }
+};
+
+template <typename T, int R, bool EXACT>
+__global__ void __launch_bounds__(256) step2d_resident(Res2DArgs<T> a, int L, int cur0, int record) {
+    using A = Ar<T, EXACT>;
+    using S = Res2DShape<T, R>;
+    constexpr int V = S::V, TX = S::TX, HY = S::HY, UW = S::UW, HV = HY / V;
+    using VT = Vec<T, V>;
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    if (a.ctrl->abort) return;  // same value in every block: nothing here writes it
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int BZ = a.BZ, ROWS = S::rows(BZ);
+    T* const su0 = reinterpret_cast<T*>(sm_raw);
+    T* const su1 = su0 + ROWS * UW;
+    T* sc = su1 + ROWS * UW;  // c2dt2, om, iop: BZ x TX
+    T* som = sc + BZ * TX;
+    T* siop = som + BZ * TX;
+    double* prod = reinterpret_cast<double*>(siop + BZ * TX) + (threadIdx.x >> 5) * F2D_CHUNK;
+    int* stap = reinterpret_cast<int*>(reinterpret_cast<double*>(siop + BZ * TX) + 8 * F2D_CHUNK);
+
+    const int nz = a.nz, nx = a.nx;
+    const long long ld = a.ld;
+    const int bzi = blockIdx.x / a.xb, bxi = blockIdx.x % a.xb;
+    const int z0 = bzi * BZ, x0 = bxi * TX;
+    const int bz = min(BZ, nz - z0), bx = min(TX, nx - x0);  // valid rows / columns
+    const int tid = threadIdx.x, tcv = tid & 15, trow = tid >> 4;
+    const unsigned long long base = a.ctrl->step, row_base = a.ctrl->row_base;
+    auto gidx = [&](int z, int x) { return a.origin + (long long)z * ld + x; };
+    auto sidx = [&](int z, int x) { return (z - z0 + R) * UW + (x - x0 + HY); };  // smem offset of (z, x)
+    const bool top = z0 == 0, bot = z0 + bz == nz, lef = x0 == 0, rig = x0 + bx == nx;
+    auto mir = [](int f, T v) { return f == 0 ? T(0) : (f < 0 ? -v : v); };
+
+    // ---- chunk start: both levels' valid region, the current level's halo
+    // (stored ghosts on faces: a caller-uploaded level's ghosts are used as
+    // given, kernel.hpp:344-379 reads them), and the constant fields ----
+    for (int i = tid; i < ROWS * UW; i += 256) {
+        const int r = i / UW, cc = i % UW;
+        const int z = z0 - R + r, x = x0 - HY + cc;
+        const bool inz = z >= -R && z < nz + R, inx = x >= -HY && x < nx + HY;
+        T c = T(0), p = T(0);
+        const bool valid = z >= z0 && z < z0 + bz && x >= x0 && x < x0 + bx;
+        const bool halo = (z >= z0 && z < z0 + bz && ((x >= x0 - HY && x < x0) || (x >= x0 + bx && x < x0 + bx + HY))) ||
+                          (x >= x0 && x < x0 + bx && ((z >= z0 - R && z < z0) || (z >= z0 + bz && z < z0 + bz + R)));
+        if (inz && inx && (valid || halo)) c = a.lvl[cur0][gidx(z, x)];
+        if (valid) p = a.lvl[cur0 ^ 1][gidx(z, x)];
+        su0[i] = c;
+        su1[i] = p;
+    }
+    for (int i = tid; i < BZ * TX; i += 256) {
+        const int r = i / TX, cc = i % TX;
+        T c2 = T(0), om = T(1), iop = T(1);
+        if (r < bz && cc < bx) {
+            const long long g = gidx(z0 + r, x0 + cc);
+            c2 = a.c2dt2[g];
+            const T e = a.eta[g];
+            if (e != T(0)) damping_factors(e, a.dt, om, iop);
+        }
+        sc[i] = c2;
+        som[i] = om;
+        siop[i] = iop;
+    }
+    __syncthreads();
+
+    const int nt0 = a.blk_toff[blockIdx.x], nt1 = a.blk_toff[blockIdx.x + 1];
+    const int nr0 = a.blk_roff[blockIdx.x], nr1 = a.blk_roff[blockIdx.x + 1];
+    const bool tap_cached = record && nr1 - nr0 <= a.tapcap;
+    if (tap_cached)
+        for (int q = nr0 + tid; q < nr1; q += 256) stap[q - nr0] = a.blk_rpack[q];
+    const int lane = tid & 31, wib = tid >> 5;
+    // Receivers (acquisition.hpp:150-161): receiver r belongs to CTA r % grid,
+    // warp r / grid, so every CTA carries an equal share.  The taps of row k
+    // are loaded at the start of step k+1 and summed after its compute, so the
+    // L2 latency hides behind the sweep; lane 0 sums in entry order (double,
+    // no FMA), exactly the reference's association.
+    constexpr int TPL = F2D_CHUNK / 32;  // taps per lane on the fast path
+    const int r_fast = (int)blockIdx.x + (int)gridDim.x * wib;
+    const bool has_fast = record && r_fast < a.n_rec;
+    unsigned rb = 0, re = 0;
+    double wv[TPL];
+    int ti[TPL];
+    if (has_fast) {
+        rb = a.roff[r_fast];
+        re = a.roff[r_fast + 1];
+#pragma unroll
+        for (int q = 0; q < TPL; ++q) {
+            const unsigned kk = rb + (unsigned)(q * 32 + lane);
+            wv[q] = kk < re ? a.rw[kk] : 0.0;
+            ti[q] = kk < re ? a.tap_ix[kk] : 0;
+        }
+    }
+    const bool fast_ok = re - rb <= (unsigned)F2D_CHUNK;
+    auto rec_slow = [&](int rcv, const T* tb, unsigned long long row) {  // any tap count, global loads
+        const unsigned b0 = a.roff[rcv], e = a.roff[rcv + 1];
+        double acc = 0.0;
+        for (unsigned c0 = b0; c0 < e; c0 += F2D_CHUNK) {
+            const int m = (int)min((unsigned)F2D_CHUNK, e - c0);
+#pragma unroll
+            for (int q = 0; q < TPL; ++q) {
+                const int kk = q * 32 + lane;
+                if (kk < m) prod[kk] = __dmul_rn(a.rw[c0 + kk], static_cast<double>(__ldcg(tb + a.tap_ix[c0 + kk])));
+            }
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll 8
+                for (int kk = 0; kk < m; ++kk) acc = __dadd_rn(acc, prod[kk]);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) a.seis[row * (unsigned long long)a.n_rec + rcv] = acc;
+    };
+    // row of the state after step kk of this chunk
+    auto rec_row = [&](int kk) { return base + (unsigned long long)kk + 1 - row_base; };
+
+    for (int k = 0; k < L; ++k) {
+        const T* U = (k & 1) ? su1 : su0;
+        T* O = (k & 1) ? su0 : su1;
+        T* gout = a.lvl[cur0 ^ (k & 1) ^ 1];
+        const unsigned long long n = base + (unsigned long long)k;
+        // ---- taps of the previous step's row, in flight during the sweep ----
+        T tv[TPL];
+        const bool rec_prev = record && k > 0 && rec_row(k - 1) < a.n_rows;
+        if (rec_prev && has_fast && fast_ok) {
+            const T* tb = a.tapbuf + (size_t)((k - 1) & 1) * a.n_ent;
+#pragma unroll
+            for (int q = 0; q < TPL; ++q) {
+                const unsigned kk = rb + (unsigned)(q * 32 + lane);
+                tv[q] = kk < re ? __ldcg(tb + ti[q]) : T(0);
+            }
+        }
+        // ---- sweep of the block (valid points only) ----
+        for (int r = trow; r < bz; r += 16) {
+            const int xc = tcv * V;
+            if (xc >= bx) continue;
+            const int o = (r + R) * UW + HY + xc;
+            const VT c = *reinterpret_cast<const VT*>(U + o);
+            T lz[V], lx[V], res[V];
+#pragma unroll
+            for (int e = 0; e < V; ++e) lz[e] = lx[e] = A::mul(a.v[0], c.e[e]);
+            T w[2 * HY + V];
+#pragma unroll
+            for (int q = 0; q < 2 * HV + 1; ++q) {
+                const VT t = *reinterpret_cast<const VT*>(U + o - HY + q * V);
+#pragma unroll
+                for (int e = 0; e < V; ++e) w[q * V + e] = t.e[e];
+            }
+#pragma unroll
+            for (int j = 1; j <= R; ++j) {
+                const VT zp = *reinterpret_cast<const VT*>(U + o + j * UW);
+                const VT zm = *reinterpret_cast<const VT*>(U + o - j * UW);
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    lz[e] = A::add(lz[e], A::mul(a.v[j], A::add(zp.e[e], zm.e[e])));
+                    lx[e] = A::add(lx[e], A::mul(a.v[j], A::add(w[HY + e + j], w[HY + e - j])));
+                }
+            }
+            const int po = r * TX + xc;
+            const VT pv = *reinterpret_cast<const VT*>(O + o);
+            const VT cv = *reinterpret_cast<const VT*>(sc + po);
+            const VT omv = *reinterpret_cast<const VT*>(som + po);
+            const VT iov = *reinterpret_cast<const VT*>(siop + po);
+            const int z = z0 + r;
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const T rhs = A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1]));
+                const T t = A::add(A::mul(cv.e[e], rhs), A::mul(T(2), c.e[e]));
+                // time_update (kernel.hpp:418-420): om = iop = 1 where eta = 0, exact identities
+                res[e] = A::mul(A::sub(t, A::mul(omv.e[e], pv.e[e])), iov.e[e]);
+                const int x = x0 + xc + e;
+                if ((z == 0 && a.gf[0][0] < 0) || (z == nz - 1 && a.gf[0][1] < 0) || (x == 0 && a.gf[1][0] < 0) ||
+                    (x == nx - 1 && a.gf[1][1] < 0))
+                    res[e] = T(0);  // null-Dirichlet face nodes (kernel.hpp:87-88)
+            }
+            if (xc + V <= bx) {
+                VT rv;
+#pragma unroll
+                for (int e = 0; e < V; ++e) rv.e[e] = res[e];
+                *reinterpret_cast<VT*>(O + o) = rv;
+            } else {
+                for (int e = 0; e < V && xc + e < bx; ++e) O[o + e] = res[e];
+            }
+        }
+        __syncthreads();
+        // ---- point sources of the block, entries in the reference's order ----
+        if (nt1 > nt0) {
+            if (n < a.n_wavelet) {
+                using AX = Ar<T, true>;
+                const double amp = a.wavelet[n];
+                for (int q = nt0 + tid; q < nt1; q += 256) {
+                    const int t = a.blk_tgt[q], so = a.blk_tpos[q];
+                    const int r = so / UW - R, cc = so % UW - HY;
+                    const T c2 = sc[r * TX + cc], iop = siop[r * TX + cc];
+                    T val = O[so];
+                    for (unsigned e = a.ent_off[t]; e < a.ent_off[t + 1]; ++e)
+                        val = AX::add(val, AX::mul(AX::mul(c2, static_cast<T>(__dmul_rn(a.ent_w[e], amp))), iop));
+                    O[so] = val;
+                }
+            }
+            __syncthreads();
+        }
+        // ---- boundary strips to global (the neighbours' halos), receiver taps ----
+        {
+            // top / bottom R rows (valid columns), if a neighbour reads them
+            for (int i = tid; i < R * TX; i += 256) {
+                const int rr = i / TX, cc = i % TX;
+                if (cc >= bx) continue;
+                if (!top) gout[gidx(z0 + rr, x0 + cc)] = O[sidx(z0 + rr, x0 + cc)];
+                if (!bot) gout[gidx(z0 + bz - R + rr, x0 + cc)] = O[sidx(z0 + bz - R + rr, x0 + cc)];
+            }
+            // left / right HY columns (valid rows), whole vectors
+            for (int i = tid; i < 2 * HV * BZ; i += 256) {
+                const int side = i / (HV * BZ), rem = i % (HV * BZ), rr = rem / HV, q = rem % HV;
+                if (rr >= bz || (side == 0 && lef) || (side == 1 && rig)) continue;
+                const int z = z0 + rr, x = side == 0 ? x0 + q * V : x0 + TX - HY + q * V;
+                *reinterpret_cast<VT*>(gout + gidx(z, x)) = *reinterpret_cast<const VT*>(O + sidx(z, x));
+            }
+            if (record) {
+                T* tb = a.tapbuf + (size_t)(k & 1) * a.n_ent;
+#pragma unroll 4
+                for (int q = nr0 + tid; q < nr1; q += 256) {
+                    const int pk = tap_cached ? stap[q - nr0] : a.blk_rpack[q];
+                    tb[q] = mir((pk & 3) - 1, O[pk >> 2]);
+                }
+            }
+        }
+        // ---- the previous step's row (its taps were loaded before the sweep) ----
+        if (rec_prev) {
+            const unsigned long long row = rec_row(k - 1);
+            const T* tb = a.tapbuf + (size_t)((k - 1) & 1) * a.n_ent;
+            if (has_fast && fast_ok) {
+                const int m = (int)(re - rb);
+#pragma unroll
+                for (int q = 0; q < TPL; ++q) {
+                    const int kk = q * 32 + lane;
+                    if (kk < m) prod[kk] = __dmul_rn(wv[q], static_cast<double>(tv[q]));
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    double acc = 0.0;
+#pragma unroll 8
+                    for (int kk = 0; kk < m; ++kk) acc = __dadd_rn(acc, prod[kk]);
+                    a.seis[row * (unsigned long long)a.n_rec + r_fast] = acc;
+                }
+                __syncwarp();
+            } else if (has_fast) {
+                rec_slow(r_fast, tb, row);
+            }
+            for (int rcv = r_fast + (int)gridDim.x * 8; rcv < a.n_rec; rcv += (int)gridDim.x * 8)
+                rec_slow(rcv, tb, row);
+        }
+        grid.sync();
+        // ---- halo of the new level: neighbours' strips from global ----
+        for (int i = tid; i < R * TX; i += 256) {
+            const int rr = i / TX, cc = i % TX;
+            if (cc >= bx) continue;
+            T a0 = T(0), a1 = T(0);
+            if (!top) a0 = __ldcg(gout + gidx(z0 - R + rr, x0 + cc));
+            if (!bot) a1 = __ldcg(gout + gidx(z0 + bz + rr, x0 + cc));
+            if (!top) O[sidx(z0 - R + rr, x0 + cc)] = a0;
+            if (!bot) O[sidx(z0 + bz + rr, x0 + cc)] = a1;
+        }
+        for (int i = tid; i < HV * BZ; i += 256) {
+            const int rr = i / HV, q = i % HV;
+            if (rr >= bz) continue;
+            const int z = z0 + rr;
+            // left: whole vectors of the left neighbour's strip; right: this
+            // block is full width (bx == TX) whenever a right neighbour exists
+            VT l, r;
+            if (!lef) l = ldcg16(gout + gidx(z, x0 - HY + q * V));
+            if (!rig) r = ldcg16(gout + gidx(z, x0 + TX + q * V));
+            if (!lef) *reinterpret_cast<VT*>(O + sidx(z, x0 - HY + q * V)) = l;
+            if (!rig) *reinterpret_cast<VT*>(O + sidx(z, x0 + TX + q * V)) = r;
+        }
+        __syncthreads();
+        // ---- physical faces: the new level's ghosts mirror the block
+        // (apply_boundary, kernel.hpp:84-97; Z then X; corners never read) ----
+        if (top || bot)
+            for (int i = tid; i < R * TX; i += 256) {
+                const int kk = i / TX + 1, cc = i % TX;
+                if (cc >= bx) continue;
+                if (top) O[sidx(-kk, x0 + cc)] = mir(a.gf[0][0], O[sidx(kk, x0 + cc)]);
+                if (bot) O[sidx(nz - 1 + kk, x0 + cc)] = mir(a.gf[0][1], O[sidx(nz - 1 - kk, x0 + cc)]);
+            }
+        if (lef || rig)
+            for (int i = tid; i < R * BZ; i += 256) {
+                const int kk = i % R + 1, rr = i / R;
+                if (rr >= bz) continue;
+                const int z = z0 + rr;
+                if (lef) O[sidx(z, -kk)] = mir(a.gf[1][0], O[sidx(z, kk)]);
+                if (rig) O[sidx(z, nx - 1 + kk)] = mir(a.gf[1][1], O[sidx(z, nx - 1 - kk)]);
+            }
+        __syncthreads();
+    }
+    // ---- the last step's row (its taps are complete after the last barrier) ----
+    if (record && L > 0 && rec_row(L - 1) < a.n_rows) {
+        const T* tb = a.tapbuf + (size_t)((L - 1) & 1) * a.n_ent;
+        for (int rcv = r_fast; rcv < a.n_rec; rcv += (int)gridDim.x * 8) rec_slow(rcv, tb, rec_row(L - 1));
+    }
+    // ---- chunk end: both levels' valid region and face ghosts back to global ----
+    for (int s2 = 0; s2 < 2; ++s2) {
+        T* g = a.lvl[cur0 ^ s2];
+        const T* Ls = s2 ? su1 : su0;
+        for (int i = tid; i < bz * bx; i += 256) {
+            const int z = z0 + i / bx, x = x0 + i % bx;
+            g[gidx(z, x)] = Ls[sidx(z, x)];
+        }
+        if (top || bot)
+            for (int i = tid; i < 2 * R * bx; i += 256) {
+                const int side = i / (R * bx), rem = i % (R * bx), kk = rem / bx + 1, x = x0 + rem % bx;
+                if (side == 0 && top) g[gidx(-kk, x)] = Ls[sidx(-kk, x)];
+                if (side == 1 && bot) g[gidx(nz - 1 + kk, x)] = Ls[sidx(nz - 1 + kk, x)];
+            }
+        if (lef || rig)
+            for (int i = tid; i < 2 * R * bz; i += 256) {
+                const int side = i / (R * bz), rem = i % (R * bz), kk = rem / bz + 1, z = z0 + rem % bz;
+                if (side == 0 && lef) g[gidx(z, -kk)] = Ls[sidx(z, -kk)];
+                if (side == 1 && rig) g[gidx(z, nx - 1 + kk)] = Ls[sidx(z, nx - 1 + kk)];
+            }
+    }
 }
 
 // ---------------------------------------------------------------------------
