@@ -75,3 +75,94 @@ def test_peer_transport_slabs_bit_exact_on_one_gpu():
                        timeout=900, cwd=os.path.dirname(HERE))
     assert r.returncode == 0 and "peer all ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("peer ok") == 4, r.stdout
+
+
+CHILD2 = r'''
+import os, sys, threading
+root = os.path.dirname({here!r})
+for p in (root, os.path.join(root, "oracle"), {here!r}):
+    sys.path.insert(0, p)
+import numpy as np
+from helpers import D, N, X, gpu_solver, oracle_solver, same, small_config
+from paper_2201_05278_b200 import InstabilityError, ModulatedField
+from paper_2201_05278_b200.configs import build_workload
+
+def run_ranks(fn, world):
+    out, err = [None] * world, []
+    def go(r):
+        try:
+            out[r] = fn(r)
+        except Exception as e:
+            out[r] = e
+    th = [threading.Thread(target=go, args=(r,)) for r in range(world)]
+    for t in th: t.start()
+    for t in th: t.join(120)
+    return out
+
+# 1. volume sources (the push kernel carries the halo planes after them)
+h = 20.0
+cfg = small_config(ndim=3, order=8, shape=(31, 21, 19), bc=[[N, D], [D, D], [D, N]], tf=0.05)
+w = build_workload(cfg, np.float32)
+rng = np.random.default_rng(7)
+field = rng.standard_normal(w.velocity.shape).astype(np.float32)
+amp = list(np.sin(np.arange(w.axis.n_steps + 1) * 0.3))
+world = 2
+ws = [build_workload(cfg, np.float32, rank=r, world=world) for r in range(world)]
+ss = [gpu_solver(x, slab=(*x.slab, None)) for x in ws]
+for s, x in zip(ss, ws):
+    s.set_sources(x.sources, x.wavelet)
+    zb, ze = x.slab[2], x.slab[3]
+    s.add_volume_source(ModulatedField(field=np.ascontiguousarray(field[zb:ze + 2 * w.grid.halo]), amplitude=amp))
+for s in ss:
+    s.peer_link(ss)
+out = run_ranks(lambda r: ss[r].forward(), world)
+assert all(not isinstance(o, Exception) for o in out), out
+full = np.concatenate([o.snapshots[-1] for o in out], axis=0)
+o = oracle_solver(w)
+o.set_sources(w.sources, w.wavelet)
+o.add_volume_source(field, amp)
+ref = o.forward()
+assert np.abs(ref["final"]).max() > 0
+assert same(full, ref["final"]), float(np.abs(full - ref["final"]).max())
+for s in ss: s.close()
+print("peer volume ok", flush=True)
+
+# 2. an instability: every rank stops at the oracle's step (health reduction over the sync blocks)
+cfg = small_config(ndim=3, order=2, shape=(23, 15, 15), damping_cells=0, tf=0.5, bc=[[D, D], [D, D], [D, D]])
+w = build_workload(cfg, np.float32)
+w.axis.dt *= 1.5
+w.axis.n_steps = 1000
+w.wavelet = np.resize(w.wavelet, 1001)
+o = oracle_solver(w)
+o.set_sources(w.sources, w.wavelet)
+bad = None
+for _ in range(1000):
+    bad = o.step()
+    if bad:
+        break
+assert bad is not None
+ws = []
+for r in range(world):
+    x = build_workload(cfg, np.float32, rank=r, world=world)
+    x.axis.dt, x.axis.n_steps, x.wavelet = w.axis.dt, 1000, w.wavelet
+    ws.append(x)
+ss = [gpu_solver(x, slab=(*x.slab, None)) for x in ws]
+for s, x in zip(ss, ws):
+    s.set_sources(x.sources, x.wavelet)
+for s in ss:
+    s.peer_link(ss)
+out = run_ranks(lambda r: ss[r].advance_raw(1000), world)
+for e in out:
+    assert isinstance(e, InstabilityError), out
+    assert e.step() == bad[0], (e.step(), bad[0])
+for s in ss:
+    assert s.step_index() == bad[0]
+    s.close()
+print("peer instability ok", flush=True)
+'''
+
+
+def test_peer_transport_volume_sources_and_instability():
+    r = subprocess.run([sys.executable, "-c", CHILD2.format(here=HERE)], capture_output=True, text=True,
+                       timeout=900, cwd=os.path.dirname(HERE))
+    assert r.returncode == 0 and "peer instability ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
