@@ -188,6 +188,8 @@ struct fdw_solver {
     // FUSED2D, shared-memory resident kernel (constant density): block rows,
     // blocks per grid row, blocks, dynamic smem; per-block source / tap lists
     bool res2d = false;
+    bool res_pair = false;  // two steps per grid barrier (step2d_resident2)
+    size_t res_smem2 = 0, res_smem2_base = 0;
     int res_BZ = 0, res_xb = 0, res_nb = 0;
     size_t res_smem = 0;
     int* d_blk_toff = nullptr;
@@ -565,6 +567,27 @@ const void* res2d_kernel(int R, bool ex) {
     return ex ? res2d_fn<T, true>(R) : res2d_fn<T, false>(R);
 }
 
+template <typename T, bool EX>
+const void* res2d2_fn(int R) {
+#define RF2(RR) \
+    if (R == RR) return (const void*)fdw::step2d_resident2<T, RR, EX>;
+    RF2(1) RF2(2) RF2(3) RF2(4) RF2(5) RF2(6) RF2(7) RF2(8) RF2(9) RF2(10)
+#undef RF2
+    return nullptr;
+}
+
+template <typename T>
+const void* res2d2_kernel(int R, bool ex) {
+    return ex ? res2d2_fn<T, true>(R) : res2d2_fn<T, false>(R);
+}
+
+size_t res2d2_smem(const fdw_solver* c, int BZ, int tapcap) {
+    const int V = 16 / c->tsize, TX = 16 * V, R = c->R;
+    const int H1 = ((R + V - 1) / V) * V, H2 = ((2 * R + V - 1) / V) * V;
+    return (size_t)(2 * (BZ + 4 * R) * (TX + 2 * H2) + 3 * (BZ + 2 * R) * (TX + 2 * H1)) * c->tsize +
+           8 * fdw::F2D_CHUNK * sizeof(double) + (size_t)tapcap * sizeof(int);
+}
+
 template <typename T>
 fdw_status launch_res2d_t(fdw_solver* c, int L, int cur0, bool record) {
     fdw::Res2DArgs<T> a{};
@@ -606,14 +629,30 @@ fdw_status launch_res2d_t(fdw_solver* c, int L, int cur0, bool record) {
     a.n_rows = c->seis_rows;
     a.ctrl = c->ctrl;
     int rec = record && c->d_seis && c->d_tapbuf ? 1 : 0;
-    void* args[] = {&a, &L, &cur0, &rec};
-    const void* f = res2d_kernel<T>(c->R, c->d.math == FDW_MATH_EXACT);
-    if (!f) return fail(c, FDW_EINVAL, "resident 2D kernel not built for this configuration");
-    CU(cudaLaunchCooperativeKernel(f, dim3((unsigned)c->res_nb), dim3(256), args, c->res_smem, c->stream));
-    if (c->capturing)
-        ++c->capture_kernels;
-    else
-        ++c->launches;
+    const bool ex = c->d.math == FDW_MATH_EXACT;
+    int Lp = c->res_pair ? (L & ~1) : 0, k0 = 0;
+    if (Lp >= 2) {  // pairs of steps, one grid barrier each
+        void* args2[] = {&a, &Lp, &cur0, &rec};
+        const void* f2 = res2d2_kernel<T>(c->R, ex);
+        if (!f2) return fail(c, FDW_EINVAL, "resident 2D kernel not built for this configuration");
+        CU(cudaLaunchCooperativeKernel(f2, dim3((unsigned)c->res_nb), dim3(256), args2, c->res_smem2, c->stream));
+        if (c->capturing)
+            ++c->capture_kernels;
+        else
+            ++c->launches;
+        k0 = Lp;
+    }
+    int Ls = L - k0, cur = cur0 ^ (k0 & 1);
+    if (Ls > 0) {
+        void* args[] = {&a, &Ls, &cur, &rec, &k0};
+        const void* f = res2d_kernel<T>(c->R, ex);
+        if (!f) return fail(c, FDW_EINVAL, "resident 2D kernel not built for this configuration");
+        CU(cudaLaunchCooperativeKernel(f, dim3((unsigned)c->res_nb), dim3(256), args, c->res_smem, c->stream));
+        if (c->capturing)
+            ++c->capture_kernels;
+        else
+            ++c->launches;
+    }
     return FDW_OK;
 }
 
@@ -629,6 +668,43 @@ bool res2d_configure(fdw_solver* c) {
     if (nx - (long long)(xb - 1) * TX < 2 * HY) return false;
     const void* f = res2d_kernel<T>(R, c->d.math == FDW_MATH_EXACT);
     if (!f) return false;
+    // two steps per barrier: 2R strips and halos; blocks >= 2R rows, >= 2*H2 columns
+    const int H2 = ((2 * R + V - 1) / V) * V;
+    const void* f2 = res2d2_kernel<T>(R, c->d.math == FDW_MATH_EXACT);
+    if (!std::getenv("FDW_NO_RES2D_PAIR") && f2 && nx - (long long)(xb - 1) * TX >= 2 * H2) {
+        for (int occ = 3; occ >= 1; --occ) {
+            const long long cap = (long long)occ * c->sm_count;
+            const long long zbn0 = std::min<long long>(nz, cap / xb);
+            if (zbn0 < 1) continue;
+            const int BZ = (int)((nz + zbn0 - 1) / zbn0);
+            const int zbn = (int)((nz + BZ - 1) / BZ);
+            if (BZ < 2 * R || nz - (long long)(zbn - 1) * BZ < 2 * R) continue;
+            const size_t smem2 = res2d2_smem(c, BZ, 0);
+            const size_t smem1 =
+                (size_t)(2 * (BZ + 2 * R) * UW + 3 * BZ * TX) * sizeof(T) + 8 * fdw::F2D_CHUNK * sizeof(double);
+            if (smem2 > 227 * 1024) continue;
+            if (cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) != cudaSuccess ||
+                cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            int got = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&got, f2, 256, smem2) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            if ((long long)zbn * xb > (long long)got * c->sm_count) continue;
+            c->res2d = true;
+            c->res_pair = true;
+            c->res_BZ = BZ;
+            c->res_xb = xb;
+            c->res_nb = zbn * xb;
+            c->res_smem = c->res_smem_base = smem1;
+            c->res_smem2 = c->res_smem2_base = smem2;
+            c->occupancy = got;
+            return true;
+        }
+    }
     for (int occ = 3; occ >= 1; --occ) {
         const long long cap = (long long)occ * c->sm_count;
         const long long zbn0 = std::min<long long>(nz, cap / xb);
@@ -661,11 +737,12 @@ bool res2d_configure(fdw_solver* c) {
     return false;
 }
 
-// smem offset of extended (z, x) inside its block of the resident 2D kernel
+// block of extended (z, x) in the resident 2D decomposition, and its packed
+// block-local coordinates (fdw::res2d_pack)
 long long res2d_block_of(const fdw_solver* c, long long z, long long x, int* pos) {
-    const int V = 16 / c->tsize, TX = 16 * V, HY = ((c->R + V - 1) / V) * V, UW = TX + 2 * HY;
+    const int TX = 16 * (16 / c->tsize);
     const long long bz = z / c->res_BZ, bx = x / TX;
-    *pos = (int)((z - bz * c->res_BZ + c->R) * UW + (x - bx * TX + HY));
+    *pos = fdw::res2d_pack((int)(z - bz * c->res_BZ), (int)(x - bx * TX));
     return bz * c->res_xb + bx;
 }
 
@@ -1183,13 +1260,22 @@ fdw_status dev_upload(fdw_solver* c, P** dst, const std::vector<P>& v) {
 fdw_status res2d_sources(fdw_solver* c) {
     const int nb = c->res_nb;
     std::vector<std::vector<std::pair<int, int>>> per((size_t)nb);
+    const int TX = 16 * (16 / c->tsize), ring = c->res_pair ? c->R : 0;
+    const int zbn = c->res_nb / c->res_xb;
     for (size_t t = 0; t < c->h_tgt.size(); ++t) {
         const long long rem = c->h_tgt[t] - c->origin;
         const long long z = rem / c->ld, x = rem % c->ld;
         if (rem < 0 || z >= c->nzl || x >= c->nxl) return fail(c, FDW_EINVAL, "source target outside the grid");
-        int pos = 0;
-        const long long b = res2d_block_of(c, z, x, &pos);
-        per[(size_t)b].push_back({(int)t, pos});
+        // the owning block, and (two-step kernel) every block whose R-wide ring holds it
+        for (int bzi = 0; bzi < zbn; ++bzi)
+            for (int bxi = 0; bxi < c->res_xb; ++bxi) {
+                const long long z0 = (long long)bzi * c->res_BZ, x0 = (long long)bxi * TX;
+                const long long z1 = std::min<long long>(z0 + c->res_BZ, c->nzl), x1 = std::min<long long>(x0 + TX, c->nxl);
+                if (z < z0 - ring || z >= z1 + ring || x < x0 - ring || x >= x1 + ring) continue;
+                const bool in = z >= z0 && z < z1 && x >= x0 && x < x1;
+                per[(size_t)(bzi * c->res_xb + bxi)].push_back(
+                    {(int)t, fdw::res2d_pack((int)(z - z0), (int)(x - x0)) | (in ? fdw::RES2D_IN_BLOCK : 0)});
+            }
     }
     std::vector<int> off(1, 0), tg, ps;
     for (auto& v : per) {
@@ -1227,8 +1313,8 @@ fdw_status res2d_receivers(fdw_solver* c, const std::vector<long long>& ri) {
         if (x < 0) { x = -x; f *= fac(1, 0); }
         if (x >= c->nxl) { x = 2 * (c->nxl - 1) - x; f *= fac(1, 1); }
         if (z < 0 || z >= c->nzl || x < 0 || x >= c->nxl) return fail(c, FDW_EINVAL, "receiver tap outside the grid");
-        if (f == 0) {
-            per[0].push_back({e, -1, 0});
+        if (f == 0) {  // "none" face: the tap reads +0 (any in-block position, factor 0)
+            per[0].push_back({e, fdw::res2d_pack(0, 0), 0});
             continue;
         }
         int pos = 0;
@@ -1240,8 +1326,7 @@ fdw_status res2d_receivers(fdw_solver* c, const std::vector<long long>& ri) {
     for (auto& v : per) {
         for (auto& t : v) {
             ix[(size_t)std::get<0>(t)] = (int)pack.size();
-            const int pos = std::max(std::get<1>(t), 0);
-            pack.push_back((pos << 2) | (std::get<2>(t) + 1));
+            pack.push_back((std::get<1>(t) << 2) | (std::get<2>(t) + 1));
         }
         most = std::max(most, (int)v.size());
         off.push_back((int)pack.size());
@@ -1253,25 +1338,35 @@ fdw_status res2d_receivers(fdw_solver* c, const std::vector<long long>& ri) {
     // cache each block's tap list in shared memory when the grid still fits
     c->res_tapcap = 0;
     c->res_smem = c->res_smem_base;
+    c->res_smem2 = c->res_smem2_base;
     if (most > 0 && most <= 16384) {
-        const size_t smem = c->res_smem_base + (size_t)most * sizeof(int);
-        const void* f = c->tsize == 4 ? res2d_kernel<float>(c->R, c->d.math == FDW_MATH_EXACT)
-                                      : res2d_kernel<double>(c->R, c->d.math == FDW_MATH_EXACT);
-        int got = 0;
-        if (smem <= 227 * 1024 && cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
-                                      cudaSuccess &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&got, f, 256, smem) == cudaSuccess &&
-            (long long)c->res_nb <= (long long)got * c->sm_count) {
+        const bool ex = c->d.math == FDW_MATH_EXACT;
+        auto fits = [&](const void* f, size_t smem) {
+            int got = 0;
+            return smem <= 227 * 1024 &&
+                   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+                   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&got, f, 256, smem) == cudaSuccess &&
+                   (long long)c->res_nb <= (long long)got * c->sm_count;
+        };
+        const size_t s1 = c->res_smem_base + (size_t)most * sizeof(int);
+        const size_t s2 = c->res_smem2_base + (size_t)most * sizeof(int);
+        const void* f1 = c->tsize == 4 ? res2d_kernel<float>(c->R, ex) : res2d_kernel<double>(c->R, ex);
+        const void* f2 = c->tsize == 4 ? res2d2_kernel<float>(c->R, ex) : res2d2_kernel<double>(c->R, ex);
+        if (fits(f1, s1) && (!c->res_pair || fits(f2, s2))) {
             c->res_tapcap = most;
-            c->res_smem = smem;
+            c->res_smem = s1;
+            c->res_smem2 = s2;
+        } else {  // restore the attributes of the uncached sizes
+            cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem_base);
+            if (c->res_pair) cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem2_base);
         }
         cudaGetLastError();
     }
     if (c->d_tapbuf) cudaFreeAsync(c->d_tapbuf, c->stream);
     c->d_tapbuf = nullptr;
     c->n_ent = n;
-    CU(cudaMallocAsync(&c->d_tapbuf, (size_t)std::max(1, 2 * n) * c->tsize, c->stream));
-    CU(cudaMemsetAsync(c->d_tapbuf, 0, (size_t)std::max(1, 2 * n) * c->tsize, c->stream));
+    CU(cudaMallocAsync(&c->d_tapbuf, (size_t)std::max(1, 4 * n) * c->tsize, c->stream));  // 4 rows in flight
+    CU(cudaMemsetAsync(c->d_tapbuf, 0, (size_t)std::max(1, 4 * n) * c->tsize, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     return FDW_OK;
 }

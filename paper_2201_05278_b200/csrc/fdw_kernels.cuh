@@ -1034,7 +1034,9 @@ struct Res2DArgs {
     int nz, nx;
     int gf[2][2];        // mirror factor per face: -1 Dirichlet, +1 Neumann, 0 none
     int BZ, xb;          // block rows; blocks per grid row (block b = zb_idx * xb + xb_idx)
-    // point sources: per-block CSR (targets, smem offset r*UW+c) over the merged targets
+    // point sources: per-block CSR over the merged targets: target index and
+    // res2d_pack(rr, cc) block-local coordinates (bit 22: inside the block;
+    // otherwise in its R-wide ring, used by the two-step kernel)
     const int* blk_toff;
     const int* blk_tgt;
     const int* blk_tpos;
@@ -1042,7 +1044,7 @@ struct Res2DArgs {
     const double* ent_w;
     const double* wavelet;
     unsigned long long n_wavelet;
-    // receivers: per-block CSR of taps, packed (smem offset << 2 | factor + 1);
+    // receivers: per-block CSR of taps, packed (res2d_pack(rr, cc) << 2 | factor + 1);
     // tap q of the concatenated lists goes to tapbuf[q]; entry e reads tap_ix[e]
     const int* blk_roff;
     const int* blk_rpack;
@@ -1058,6 +1060,12 @@ struct Res2DArgs {
     Ctrl* ctrl;
 };
 
+// block-local coordinates (rr, cc in [-512, 1536)) packed into 22 bits
+__host__ __device__ __forceinline__ int res2d_pack(int rr, int cc) { return ((rr + 512) << 11) | (cc + 512); }
+__host__ __device__ __forceinline__ int res2d_rr(int pk) { return ((pk >> 11) & 2047) - 512; }
+__host__ __device__ __forceinline__ int res2d_cc(int pk) { return (pk & 2047) - 512; }
+constexpr int RES2D_IN_BLOCK = 1 << 22;
+
 template <typename T, int R>
 struct Res2DShape {
     static constexpr int V = 16 / (int)sizeof(T);
@@ -1072,7 +1080,7 @@ struct Res2DShape {
 };
 
 template <typename T, int R, bool EXACT>
-__global__ void __launch_bounds__(256) step2d_resident(Res2DArgs<T> a, int L, int cur0, int record) {
+__global__ void __launch_bounds__(256) step2d_resident(Res2DArgs<T> a, int L, int cur0, int record, int k0) {
     using A = Ar<T, EXACT>;
     using S = Res2DShape<T, R>;
     constexpr int V = S::V, TX = S::TX, HY = S::HY, UW = S::UW, HV = HY / V;
@@ -1096,7 +1104,8 @@ __global__ void __launch_bounds__(256) step2d_resident(Res2DArgs<T> a, int L, in
     const int z0 = bzi * BZ, x0 = bxi * TX;
     const int bz = min(BZ, nz - z0), bx = min(TX, nx - x0);  // valid rows / columns
     const int tid = threadIdx.x, tcv = tid & 15, trow = tid >> 4;
-    const unsigned long long base = a.ctrl->step, row_base = a.ctrl->row_base;
+    // k0: steps of this chunk already taken by an earlier launch (two-step kernel)
+    const unsigned long long base = a.ctrl->step + (unsigned long long)k0, row_base = a.ctrl->row_base;
     auto gidx = [&](int z, int x) { return a.origin + (long long)z * ld + x; };
     auto sidx = [&](int z, int x) { return (z - z0 + R) * UW + (x - x0 + HY); };  // smem offset of (z, x)
     const bool top = z0 == 0, bot = z0 + bz == nz, lef = x0 == 0, rig = x0 + bx == nx;
@@ -1258,8 +1267,9 @@ __global__ void __launch_bounds__(256) step2d_resident(Res2DArgs<T> a, int L, in
                 using AX = Ar<T, true>;
                 const double amp = a.wavelet[n];
                 for (int q = nt0 + tid; q < nt1; q += 256) {
-                    const int t = a.blk_tgt[q], so = a.blk_tpos[q];
-                    const int r = so / UW - R, cc = so % UW - HY;
+                    const int t = a.blk_tgt[q], pk = a.blk_tpos[q];
+                    if (!(pk & RES2D_IN_BLOCK)) continue;  // ring target (two-step kernel only)
+                    const int r = res2d_rr(pk), cc = res2d_cc(pk), so = (r + R) * UW + (cc + HY);
                     const T c2 = sc[r * TX + cc], iop = siop[r * TX + cc];
                     T val = O[so];
                     for (unsigned e = a.ent_off[t]; e < a.ent_off[t + 1]; ++e)
@@ -1290,7 +1300,8 @@ __global__ void __launch_bounds__(256) step2d_resident(Res2DArgs<T> a, int L, in
 #pragma unroll 4
                 for (int q = nr0 + tid; q < nr1; q += 256) {
                     const int pk = tap_cached ? stap[q - nr0] : a.blk_rpack[q];
-                    tb[q] = mir((pk & 3) - 1, O[pk >> 2]);
+                    const int c = pk >> 2;
+                    tb[q] = mir((pk & 3) - 1, O[(res2d_rr(c) + R) * UW + res2d_cc(c) + HY]);
                 }
             }
         }
@@ -1386,6 +1397,363 @@ __global__ void __launch_bounds__(256) step2d_resident(Res2DArgs<T> a, int L, in
                 const int side = i / (R * bz), rem = i % (R * bz), kk = rem / bz + 1, z = z0 + rem % bz;
                 if (side == 0 && lef) g[gidx(z, -kk)] = Ls[sidx(z, -kk)];
                 if (side == 1 && rig) g[gidx(z, nx - 1 + kk)] = Ls[sidx(z, nx - 1 + kk)];
+            }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Two steps per grid barrier (step2d_resident2): each block also computes the
+// first step of a pair on an R-wide ring around itself (the neighbours'
+// points, recomputed with the same operations and inputs, so bit-identical),
+// which lets the second step run without an exchange.  Per pair the blocks
+// exchange a 2R-wide halo of the newest level (corners included) and keep the
+// ring of the intermediate level as the next pair's "previous" level.
+// Odd chunk lengths finish with one step2d_resident launch.
+template <typename T, int R>
+struct Res2DShape2 {
+    static constexpr int V = 16 / (int)sizeof(T);
+    static constexpr int TX = 16 * V;
+    static constexpr int H1 = ((R + V - 1) / V) * V;      // ring columns, whole vectors
+    static constexpr int H2 = ((2 * R + V - 1) / V) * V;  // halo columns of the level slots
+    static constexpr int UW = TX + 2 * H2;                // slot row pitch
+    static constexpr int CW = TX + 2 * H1;                // coefficient row pitch (block + ring)
+    static constexpr int NV1 = CW / V;                    // vectors per ring row
+    static __host__ __device__ constexpr size_t smem(int BZ, int tapcap = 0) {
+        return (size_t)(2 * (BZ + 4 * R) * UW + 3 * (BZ + 2 * R) * CW) * sizeof(T) +
+               8 * F2D_CHUNK * sizeof(double) + (size_t)tapcap * sizeof(int);
+    }
+};
+
+template <typename T, int R, bool EXACT>
+__global__ void __launch_bounds__(256) step2d_resident2(Res2DArgs<T> a, int L, int cur0, int record) {
+    using A = Ar<T, EXACT>;
+    using S = Res2DShape2<T, R>;
+    constexpr int V = S::V, TX = S::TX, H1 = S::H1, H2 = S::H2, UW = S::UW, CW = S::CW;
+    constexpr int HV = ((R + V - 1) / V);  // x-window vectors each side for the stencil
+    constexpr int HW = HV * V;
+    using VT = Vec<T, V>;
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    if (a.ctrl->abort) return;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int BZ = a.BZ, ROWS = BZ + 4 * R, CROWS = BZ + 2 * R;
+    T* const sU = reinterpret_cast<T*>(sm_raw);  // current level (2R halo)
+    T* const sO = sU + ROWS * UW;                // previous / intermediate level (R ring)
+    T* const sc = sO + ROWS * UW;                // c2dt2, om, iop on the block + ring
+    T* const som = sc + CROWS * CW;
+    T* const siop = som + CROWS * CW;
+    double* prod = reinterpret_cast<double*>(siop + CROWS * CW) + (threadIdx.x >> 5) * F2D_CHUNK;
+    int* stap = reinterpret_cast<int*>(reinterpret_cast<double*>(siop + CROWS * CW) + 8 * F2D_CHUNK);
+
+    const int nz = a.nz, nx = a.nx;
+    const long long ld = a.ld;
+    const int bzi = blockIdx.x / a.xb, bxi = blockIdx.x % a.xb;
+    const int z0 = bzi * BZ, x0 = bxi * TX;
+    const int bz = min(BZ, nz - z0), bx = min(TX, nx - x0);
+    const int tid = threadIdx.x;
+    const unsigned long long base = a.ctrl->step, row_base = a.ctrl->row_base;
+    auto gidx = [&](int z, int x) { return a.origin + (long long)z * ld + x; };
+    auto sidx = [&](int z, int x) { return (z - z0 + 2 * R) * UW + (x - x0 + H2); };
+    auto cidx = [&](int z, int x) { return (z - z0 + R) * CW + (x - x0 + H1); };
+    const bool top = z0 == 0, bot = z0 + bz == nz, lef = x0 == 0, rig = x0 + bx == nx;
+    auto mir = [](int f, T v) { return f == 0 ? T(0) : (f < 0 ? -v : v); };
+    // ring extent inside the grid
+    const int rz0 = max(z0 - R, 0), rz1 = min(z0 + bz + R, nz);
+    const int rx0 = max(x0 - R, 0), rx1 = min(x0 + bx + R, nx);
+
+    // ---- chunk start: current level with its 2R halo (stored ghosts on the
+    // faces), previous level and the coefficients on the block + ring ----
+    for (int i = tid; i < ROWS * UW; i += 256) {
+        const int z = z0 - 2 * R + i / UW, x = x0 - H2 + i % UW;
+        T c = T(0), p = T(0);
+        if (z >= -R && z < nz + R && x >= -H2 && x < nx + H2) c = a.lvl[cur0][gidx(z, x)];
+        if (z >= rz0 && z < rz1 && x >= rx0 && x < rx1) p = a.lvl[cur0 ^ 1][gidx(z, x)];
+        sU[i] = c;
+        sO[i] = p;
+    }
+    for (int i = tid; i < CROWS * CW; i += 256) {
+        const int z = z0 - R + i / CW, x = x0 - H1 + i % CW;
+        T c2 = T(0), om = T(1), iop = T(1);
+        if (z >= 0 && z < nz && x >= 0 && x < nx) {
+            const long long g = gidx(z, x);
+            c2 = a.c2dt2[g];
+            const T e = a.eta[g];
+            if (e != T(0)) damping_factors(e, a.dt, om, iop);
+        }
+        sc[i] = c2;
+        som[i] = om;
+        siop[i] = iop;
+    }
+    const int nt0 = a.blk_toff[blockIdx.x], nt1 = a.blk_toff[blockIdx.x + 1];
+    const int nr0 = a.blk_roff[blockIdx.x], nr1 = a.blk_roff[blockIdx.x + 1];
+    const bool tap_cached = record && nr1 - nr0 <= a.tapcap;
+    if (tap_cached)
+        for (int q = nr0 + tid; q < nr1; q += 256) stap[q - nr0] = a.blk_rpack[q];
+    __syncthreads();
+
+    const int lane = tid & 31, wib = tid >> 5;
+    constexpr int TPL = F2D_CHUNK / 32;
+    const int r_fast = (int)blockIdx.x + (int)gridDim.x * wib;
+    const bool has_fast = record && r_fast < a.n_rec;
+    unsigned rb = 0, re = 0;
+    double wv[TPL];
+    int ti[TPL];
+    if (has_fast) {
+        rb = a.roff[r_fast];
+        re = a.roff[r_fast + 1];
+#pragma unroll
+        for (int q = 0; q < TPL; ++q) {
+            const unsigned kk = rb + (unsigned)(q * 32 + lane);
+            wv[q] = kk < re ? a.rw[kk] : 0.0;
+            ti[q] = kk < re ? a.tap_ix[kk] : 0;
+        }
+    }
+    const bool fast_ok = re - rb <= (unsigned)F2D_CHUNK;
+    auto rec_slow = [&](int rcv, const T* tb, unsigned long long row) {
+        const unsigned b0 = a.roff[rcv], e = a.roff[rcv + 1];
+        double acc = 0.0;
+        for (unsigned c0 = b0; c0 < e; c0 += F2D_CHUNK) {
+            const int m = (int)min((unsigned)F2D_CHUNK, e - c0);
+#pragma unroll
+            for (int q = 0; q < TPL; ++q) {
+                const int kk = q * 32 + lane;
+                if (kk < m) prod[kk] = __dmul_rn(a.rw[c0 + kk], static_cast<double>(__ldcg(tb + a.tap_ix[c0 + kk])));
+            }
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll 8
+                for (int kk = 0; kk < m; ++kk) acc = __dadd_rn(acc, prod[kk]);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) a.seis[row * (unsigned long long)a.n_rec + rcv] = acc;
+    };
+    auto rec_fast = [&](const T (&tv)[TPL], unsigned long long row) {
+        const int m = (int)(re - rb);
+#pragma unroll
+        for (int q = 0; q < TPL; ++q) {
+            const int kk = q * 32 + lane;
+            if (kk < m) prod[kk] = __dmul_rn(wv[q], static_cast<double>(tv[q]));
+        }
+        __syncwarp();
+        if (lane == 0) {
+            double acc = 0.0;
+#pragma unroll 8
+            for (int kk = 0; kk < m; ++kk) acc = __dadd_rn(acc, prod[kk]);
+            a.seis[row * (unsigned long long)a.n_rec + r_fast] = acc;
+        }
+        __syncwarp();
+    };
+    auto rec_row = [&](int kk) { return base + (unsigned long long)kk + 1 - row_base; };
+    auto tslot = [&](int kk) { return a.tapbuf + (size_t)(kk & 3) * a.n_ent; };  // 4 rows in flight
+
+    // one step on the region [zA, zB) x vectors [vx0, vx1) (block-local vector
+    // index, 0 = column x0 - H1): out <- in / prev, coefficient arrays at cidx
+    auto sweep = [&](const T* In, T* Out, int zA, int zB, int vx0, int vx1, int xlo, int xhi) {
+        const int nvr = vx1 - vx0;
+        for (int it = tid; it < (zB - zA) * nvr; it += 256) {
+            const int z = zA + it / nvr, xv = x0 - H1 + (vx0 + it % nvr) * V;
+            if (xv + V <= xlo || xv >= xhi) continue;
+            const int o = sidx(z, xv);
+            const VT c = *reinterpret_cast<const VT*>(In + o);
+            T lz[V], lx[V], res[V];
+#pragma unroll
+            for (int e = 0; e < V; ++e) lz[e] = lx[e] = A::mul(a.v[0], c.e[e]);
+            T w[2 * HW + V];
+#pragma unroll
+            for (int q = 0; q < 2 * HV + 1; ++q) {
+                const VT t = *reinterpret_cast<const VT*>(In + o - HW + q * V);
+#pragma unroll
+                for (int e = 0; e < V; ++e) w[q * V + e] = t.e[e];
+            }
+#pragma unroll
+            for (int j = 1; j <= R; ++j) {
+                const VT zp = *reinterpret_cast<const VT*>(In + o + j * UW);
+                const VT zm = *reinterpret_cast<const VT*>(In + o - j * UW);
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    lz[e] = A::add(lz[e], A::mul(a.v[j], A::add(zp.e[e], zm.e[e])));
+                    lx[e] = A::add(lx[e], A::mul(a.v[j], A::add(w[HW + e + j], w[HW + e - j])));
+                }
+            }
+            const int po = cidx(z, xv);
+            const VT pv = *reinterpret_cast<const VT*>(Out + o);
+            const VT cv = *reinterpret_cast<const VT*>(sc + po);
+            const VT omv = *reinterpret_cast<const VT*>(som + po);
+            const VT iov = *reinterpret_cast<const VT*>(siop + po);
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const T rhs = A::add(A::mul(lz[e], a.ih[0]), A::mul(lx[e], a.ih[1]));
+                const T t = A::add(A::mul(cv.e[e], rhs), A::mul(T(2), c.e[e]));
+                res[e] = A::mul(A::sub(t, A::mul(omv.e[e], pv.e[e])), iov.e[e]);
+                const int x = xv + e;
+                if ((z == 0 && a.gf[0][0] < 0) || (z == nz - 1 && a.gf[0][1] < 0) || (x == 0 && a.gf[1][0] < 0) ||
+                    (x == nx - 1 && a.gf[1][1] < 0))
+                    res[e] = T(0);
+            }
+            if (xv >= xlo && xv + V <= xhi) {
+                VT rv;
+#pragma unroll
+                for (int e = 0; e < V; ++e) rv.e[e] = res[e];
+                *reinterpret_cast<VT*>(Out + o) = rv;
+            } else {
+                for (int e = 0; e < V; ++e)
+                    if (xv + e >= xlo && xv + e < xhi) Out[o + e] = res[e];
+            }
+        }
+    };
+    // point sources: ring targets too when `ring` (entries in reference order)
+    auto inject = [&](T* Out, unsigned long long n, bool ring) {
+        if (nt1 > nt0) {
+            if (n < a.n_wavelet) {
+                using AX = Ar<T, true>;
+                const double amp = a.wavelet[n];
+                for (int q = nt0 + tid; q < nt1; q += 256) {
+                    const int t = a.blk_tgt[q], pk = a.blk_tpos[q];
+                    if (!ring && !(pk & RES2D_IN_BLOCK)) continue;
+                    const int z = z0 + res2d_rr(pk), x = x0 + res2d_cc(pk);
+                    const T c2 = sc[cidx(z, x)], iop = siop[cidx(z, x)];
+                    T val = Out[sidx(z, x)];
+                    for (unsigned e = a.ent_off[t]; e < a.ent_off[t + 1]; ++e)
+                        val = AX::add(val, AX::mul(AX::mul(c2, static_cast<T>(__dmul_rn(a.ent_w[e], amp))), iop));
+                    Out[sidx(z, x)] = val;
+                }
+            }
+            __syncthreads();
+        }
+    };
+    // physical faces: R-deep ghosts mirror the level over columns [cA, cB) /
+    // rows [rA, rB) (apply_boundary, kernel.hpp:84-97)
+    auto mirror = [&](T* F, int cA, int cB, int rA, int rB) {
+        if (top || bot)
+            for (int i = tid; i < R * (cB - cA); i += 256) {
+                const int kk = i / (cB - cA) + 1, x = cA + i % (cB - cA);
+                if (top) F[sidx(-kk, x)] = mir(a.gf[0][0], F[sidx(kk, x)]);
+                if (bot) F[sidx(nz - 1 + kk, x)] = mir(a.gf[0][1], F[sidx(nz - 1 - kk, x)]);
+            }
+        if (lef || rig)
+            for (int i = tid; i < R * (rB - rA); i += 256) {
+                const int kk = i % R + 1, z = rA + i / R;
+                if (lef) F[sidx(z, -kk)] = mir(a.gf[1][0], F[sidx(z, kk)]);
+                if (rig) F[sidx(z, nx - 1 + kk)] = mir(a.gf[1][1], F[sidx(z, nx - 1 - kk)]);
+            }
+    };
+    const int vr0 = (rx0 - (x0 - H1)) / V, vr1 = (rx1 - (x0 - H1) + V - 1) / V;  // ring vectors
+    const int vb0 = H1 / V, vb1 = (H1 + bx + V - 1) / V;                         // block vectors
+
+    for (int k = 0; k < L; k += 2) {  // L is even
+        const unsigned long long n1 = base + (unsigned long long)k;
+        // taps of the previous pair's two rows, in flight during the sweeps
+        T tv0[TPL], tv1[TPL];
+        const bool rec_prev = record && k > 0;
+        if (rec_prev && has_fast && fast_ok) {
+            const T* t0 = tslot(k - 2);
+            const T* t1 = tslot(k - 1);
+#pragma unroll
+            for (int q = 0; q < TPL; ++q) {
+                const unsigned kk = rb + (unsigned)(q * 32 + lane);
+                tv0[q] = kk < re ? __ldcg(t0 + ti[q]) : T(0);
+                tv1[q] = kk < re ? __ldcg(t1 + ti[q]) : T(0);
+            }
+        }
+        // step 1 on block + ring: O <- (U, prev O)
+        sweep(sU, sO, rz0, rz1, vr0, vr1, rx0, rx1);
+        __syncthreads();
+        inject(sO, n1, true);
+        mirror(sO, x0, x0 + bx, z0, z0 + bz);
+        __syncthreads();
+        // step 2 on the block: U <- (O, prev U)
+        sweep(sO, sU, z0, z0 + bz, vb0, vb1, x0, x0 + bx);
+        __syncthreads();
+        inject(sU, n1 + 1, false);
+        // 2R-wide strips of the newest level; receiver taps of both rows
+        {
+            T* g = a.lvl[cur0];
+            for (int i = tid; i < 2 * R * TX; i += 256) {
+                const int rr = i / TX, cc = i % TX;
+                if (cc >= bx) continue;
+                if (!top) g[gidx(z0 + rr, x0 + cc)] = sU[sidx(z0 + rr, x0 + cc)];
+                if (!bot) g[gidx(z0 + bz - 2 * R + rr, x0 + cc)] = sU[sidx(z0 + bz - 2 * R + rr, x0 + cc)];
+            }
+            constexpr int H2V = H2 / V;
+            for (int i = tid; i < 2 * H2V * BZ; i += 256) {
+                const int side = i / (H2V * BZ), rem = i % (H2V * BZ), rr = rem / H2V, q = rem % H2V;
+                if (rr >= bz || (side == 0 && lef) || (side == 1 && rig)) continue;
+                const int z = z0 + rr, x = side == 0 ? x0 + q * V : x0 + TX - H2 + q * V;
+                *reinterpret_cast<VT*>(g + gidx(z, x)) = *reinterpret_cast<const VT*>(sU + sidx(z, x));
+            }
+            if (record) {
+                T* t0 = tslot(k);
+                T* t1 = tslot(k + 1);
+                for (int q = nr0 + tid; q < nr1; q += 256) {
+                    const int pk = tap_cached ? stap[q - nr0] : a.blk_rpack[q];
+                    const int c = pk >> 2, f = (pk & 3) - 1;
+                    const int so = sidx(z0 + res2d_rr(c), x0 + res2d_cc(c));
+                    t0[q] = mir(f, sO[so]);
+                    t1[q] = mir(f, sU[so]);
+                }
+            }
+        }
+        // the previous pair's rows (taps loaded before the sweeps)
+        if (rec_prev) {
+            if (has_fast && fast_ok) {
+                if (rec_row(k - 2) < a.n_rows) rec_fast(tv0, rec_row(k - 2));
+                if (rec_row(k - 1) < a.n_rows) rec_fast(tv1, rec_row(k - 1));
+            } else if (has_fast) {
+                if (rec_row(k - 2) < a.n_rows) rec_slow(r_fast, tslot(k - 2), rec_row(k - 2));
+                if (rec_row(k - 1) < a.n_rows) rec_slow(r_fast, tslot(k - 1), rec_row(k - 1));
+            }
+            for (int rcv = r_fast + (int)gridDim.x * 8; rcv < a.n_rec; rcv += (int)gridDim.x * 8) {
+                if (rec_row(k - 2) < a.n_rows) rec_slow(rcv, tslot(k - 2), rec_row(k - 2));
+                if (rec_row(k - 1) < a.n_rows) rec_slow(rcv, tslot(k - 1), rec_row(k - 1));
+            }
+        }
+        grid.sync();
+        // 2R halo of the newest level (corners too): neighbours' strips
+        {
+            const T* g = a.lvl[cur0];
+            for (int i = tid; i < ROWS * (UW / V); i += 256) {
+                const int r = i / (UW / V), q = i % (UW / V);
+                const int z = z0 - 2 * R + r, x = x0 - H2 + q * V;
+                // own block (incl. its columns past nx), ghost rows / columns: skipped
+                if ((z >= z0 && z < z0 + bz && x >= x0 && x < x0 + TX) || z < 0 || z >= nz || x < 0 || x + V > nx)
+                    continue;
+                *reinterpret_cast<VT*>(sU + sidx(z, x)) = ldcg16(g + gidx(z, x));
+            }
+        }
+        __syncthreads();
+        // faces of the newest level, over the block + ring (the next step 1 reads them there)
+        mirror(sU, rx0, rx1, rz0, rz1);
+        __syncthreads();
+    }
+    // the last pair's rows
+    if (record && L >= 2) {
+        for (int rcv = r_fast; rcv < a.n_rec; rcv += (int)gridDim.x * 8) {
+            if (rec_row(L - 2) < a.n_rows) rec_slow(rcv, tslot(L - 2), rec_row(L - 2));
+            if (rec_row(L - 1) < a.n_rows) rec_slow(rcv, tslot(L - 1), rec_row(L - 1));
+        }
+    }
+    // chunk end: both levels' block and face ghosts back to global
+    for (int s2 = 0; s2 < 2; ++s2) {
+        T* g = a.lvl[cur0 ^ s2];
+        const T* F = s2 ? sO : sU;
+        for (int i = tid; i < bz * TX; i += 256) {
+            const int z = z0 + i / TX, x = x0 + i % TX;
+            if (x < x0 + bx) g[gidx(z, x)] = F[sidx(z, x)];
+        }
+        if (top || bot)
+            for (int i = tid; i < R * TX; i += 256) {
+                const int kk = i / TX + 1, x = x0 + i % TX;
+                if (x >= x0 + bx) continue;
+                if (top) g[gidx(-kk, x)] = F[sidx(-kk, x)];
+                if (bot) g[gidx(nz - 1 + kk, x)] = F[sidx(nz - 1 + kk, x)];
+            }
+        if (lef || rig)
+            for (int i = tid; i < R * BZ; i += 256) {
+                const int kk = i % R + 1, z = z0 + i / R;
+                if (z >= z0 + bz) continue;
+                if (lef) g[gidx(z, -kk)] = F[sidx(z, -kk)];
+                if (rig) g[gidx(z, nx - 1 + kk)] = F[sidx(z, nx - 1 + kk)];
             }
     }
 }
