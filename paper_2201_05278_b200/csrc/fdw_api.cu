@@ -635,6 +635,8 @@ fdw_status launch_res2d_t(fdw_solver* c, int L, int cur0, bool record) {
         void* args2[] = {&a, &Lp, &cur0, &rec};
         const void* f2 = res2d2_kernel<T>(c->R, ex);
         if (!f2) return fail(c, FDW_EINVAL, "resident 2D kernel not built for this configuration");
+        // the smem attribute is per function, shared by every context of the process
+        CU(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem2));
         CU(cudaLaunchCooperativeKernel(f2, dim3((unsigned)c->res_nb), dim3(256), args2, c->res_smem2, c->stream));
         if (c->capturing)
             ++c->capture_kernels;
@@ -647,6 +649,7 @@ fdw_status launch_res2d_t(fdw_solver* c, int L, int cur0, bool record) {
         void* args[] = {&a, &Ls, &cur, &rec, &k0};
         const void* f = res2d_kernel<T>(c->R, ex);
         if (!f) return fail(c, FDW_EINVAL, "resident 2D kernel not built for this configuration");
+        CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem));
         CU(cudaLaunchCooperativeKernel(f, dim3((unsigned)c->res_nb), dim3(256), args, c->res_smem, c->stream));
         if (c->capturing)
             ++c->capture_kernels;
@@ -672,7 +675,8 @@ bool res2d_configure(fdw_solver* c) {
     const int H2 = ((2 * R + V - 1) / V) * V;
     const void* f2 = res2d2_kernel<T>(R, c->d.math == FDW_MATH_EXACT);
     if (!std::getenv("FDW_NO_RES2D_PAIR") && f2 && nx - (long long)(xb - 1) * TX >= 2 * H2) {
-        for (int occ = 3; occ >= 1; --occ) {
+        // 2 CTAs/SM first: measured faster than 3 smaller blocks (more ring per block) on C1
+        for (int occ : {2, 3, 1}) {
             const long long cap = (long long)occ * c->sm_count;
             const long long zbn0 = std::min<long long>(nz, cap / xb);
             if (zbn0 < 1) continue;

@@ -1696,7 +1696,28 @@ __global__ void __launch_bounds__(256) step2d_resident2(Res2DArgs<T> a, int L, i
         }
         // the previous pair's rows (taps loaded before the sweeps)
         if (rec_prev) {
-            if (has_fast && fast_ok) {
+            if (has_fast && fast_ok && re - rb <= (unsigned)(F2D_CHUNK / 2) && rec_row(k - 1) < a.n_rows) {
+                // both rows at once: products in the two halves of the warp's
+                // buffer, lanes 0 and 16 run the two sequential sums side by side
+                const int m = (int)(re - rb);
+#pragma unroll
+                for (int q = 0; q < TPL; ++q) {
+                    const int kk = q * 32 + lane;
+                    if (kk < m) {
+                        prod[kk] = __dmul_rn(wv[q], static_cast<double>(tv0[q]));
+                        prod[F2D_CHUNK / 2 + kk] = __dmul_rn(wv[q], static_cast<double>(tv1[q]));
+                    }
+                }
+                __syncwarp();
+                if (lane == 0 || lane == 16) {
+                    const double* pp = prod + (lane ? F2D_CHUNK / 2 : 0);
+                    double acc = 0.0;
+#pragma unroll 8
+                    for (int kk = 0; kk < m; ++kk) acc = __dadd_rn(acc, pp[kk]);
+                    a.seis[rec_row(k - (lane ? 1 : 2)) * (unsigned long long)a.n_rec + r_fast] = acc;
+                }
+                __syncwarp();
+            } else if (has_fast && fast_ok) {
                 if (rec_row(k - 2) < a.n_rows) rec_fast(tv0, rec_row(k - 2));
                 if (rec_row(k - 1) < a.n_rows) rec_fast(tv1, rec_row(k - 1));
             } else if (has_fast) {
