@@ -143,6 +143,7 @@ struct fdw_solver {
     std::map<std::tuple<unsigned long long, int, int, int>, cudaGraphExec_t> graphs;
     std::map<std::tuple<unsigned long long, int, int, int>, unsigned long long> graph_kernels;
     bool capturing = false;
+    bool pdl_sweep = false;  // next TMA sweep launch: programmatic dependent launch (enqueue_step)
     unsigned long long capture_kernels = 0;
     unsigned long long launches = 0;  // kernels launched (graph nodes included)
     ncclComm_t comm = nullptr;
@@ -507,19 +508,29 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst, int gz 
     const CUtensorMap& g0 = c->tm_g[0];
     const CUtensorMap& g1 = c->tm_g[1];
     const CUtensorMap& g2 = c->tm_g[2];
-    switch (c->R) {
-#define LT(RR)                                                                                          \
-    case RR:                                                                                            \
-        if (c->vd)                                                                                      \
-            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2, true><<<grid, block, smem, st>>>(                    \
-                a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);                 \
-        else if (c->tma_minb == 3)                                                                      \
-            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3><<<grid, block, smem, st>>>(                          \
-                a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);                 \
-        else                                                                                            \
-            fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2><<<grid, block, smem, st>>>(                          \
-                a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);                 \
+    // programmatic dependent launch: the sweep's prologue (mbarrier setup,
+    // eta-range load) overlaps the predecessor's tail; it waits in-kernel
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = c->pdl_sweep && st == c->stream ? 1 : 0;
+    auto go = [&](auto kern) {
+        // an error is left for the caller's CHECK_LAUNCH (cudaGetLastError)
+        (void)cudaLaunchKernelEx(&cfg, kern, a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);
         return true;
+    };
+    switch (c->R) {
+#define LT(RR)                                                                 \
+    case RR:                                                                   \
+        if (c->vd) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2, true>);   \
+        if (c->tma_minb == 3) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3>); \
+        return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2>);
         LT(1)
         LT(2)
         LT(4)
@@ -941,7 +952,8 @@ fdw_status launch_sweep(fdw_solver* c, int src, int dst, bool virt) {
 }
 
 template <typename T>
-fdw_status launch_inject_t(fdw_solver* c, int dst, int k, int t0 = 0, int cnt = -1, cudaStream_t st = nullptr) {
+fdw_status launch_inject_t(fdw_solver* c, int dst, int k, int t0 = 0, int cnt = -1, cudaStream_t st = nullptr,
+                           bool pdl = false) {
     if (cnt < 0) cnt = c->n_tgt - t0;
     if (cnt <= 0) return FDW_OK;
     if (!st) st = c->stream;
@@ -955,9 +967,21 @@ fdw_status launch_inject_t(fdw_solver* c, int dst, int k, int t0 = 0, int cnt = 
         pm.lo_end = c->origin + (long long)c->R * c->plane;
         pm.hi_begin = c->origin + (c->nzl - c->R) * c->plane;
     }
-    fdw::inject_kernel<T, true><<<(cnt + tb - 1) / tb, tb, 0, st>>>(
-        static_cast<T*>(c->lvl[dst]), static_cast<const T*>(c->c2dt2), static_cast<const T*>(c->eta),
-        c->d.dt, c->d_tgt + t0, c->d_ent_off + t0, c->d_ent_w, c->d_wavelet, c->n_wavelet, cnt, k, c->ctrl, pm);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((cnt + tb - 1) / tb));
+    cfg.blockDim = dim3(tb);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;  // PDL: setup-time loads overlap the sweep's tail (inject_kernel)
+    (void)cudaLaunchKernelEx(&cfg, fdw::inject_kernel<T, true>, static_cast<T*>(c->lvl[dst]),
+                             static_cast<const T*>(c->c2dt2), static_cast<const T*>(c->eta), c->d.dt,
+                             static_cast<const long long*>(c->d_tgt + t0),
+                             static_cast<const unsigned int*>(c->d_ent_off + t0),
+                             static_cast<const double*>(c->d_ent_w), static_cast<const double*>(c->d_wavelet),
+                             c->n_wavelet, cnt, k, static_cast<const fdw::Ctrl*>(c->ctrl), pm);
     CHECK_LAUNCH();
     return FDW_OK;
 }
@@ -985,8 +1009,9 @@ fdw_status launch_volume_t(fdw_solver* c, int dst, int k) {
     return FDW_OK;
 }
 
-fdw_status launch_inject(fdw_solver* c, int dst, int k) {
-    fdw_status s = c->tsize == 4 ? launch_inject_t<float>(c, dst, k) : launch_inject_t<double>(c, dst, k);
+fdw_status launch_inject(fdw_solver* c, int dst, int k, bool pdl = false) {
+    fdw_status s = c->tsize == 4 ? launch_inject_t<float>(c, dst, k, 0, -1, nullptr, pdl)
+                                 : launch_inject_t<double>(c, dst, k, 0, -1, nullptr, pdl);
     if (s) return s;
     return c->tsize == 4 ? launch_volume_t<float>(c, dst, k) : launch_volume_t<double>(c, dst, k);
 }
@@ -1450,6 +1475,11 @@ fdw_status enqueue_split_sweep_t(fdw_solver* c, int k, int src, int dst) {
     return FDW_OK;
 }
 
+bool use_pdl(const fdw_solver* c) {
+    static const bool off = std::getenv("FDW_NO_PDL") != nullptr;
+    return !off && c->variant == FDW_KERNEL_TMA && !c->vd && c->d.world == 1 && !c->prof && c->vs_fields.empty();
+}
+
 fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
     const int dst = 1 - src;
     fdw_status s;
@@ -1461,8 +1491,13 @@ fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
         s = c->tsize == 4 ? enqueue_split_sweep_t<float>(c, k, src, dst) : enqueue_split_sweep_t<double>(c, k, src, dst);
         if (s) return s;
     } else {
-        { Mark m(c, 0); if ((s = launch_sweep(c, src, dst, virt))) return s; }
-        { Mark m(c, 1); if ((s = launch_inject(c, dst, k))) return s; }
+        // programmatic dependent launch inside a chunk (single GPU, TMA sweep
+        // on virtual ghosts, no volume sources): the sweep follows the
+        // previous step's point-source kernel, which follows this sweep
+        const bool pdl = use_pdl(c) && virt;
+        c->pdl_sweep = pdl && k > 0;
+        { Mark m(c, 0); s = launch_sweep(c, src, dst, virt); c->pdl_sweep = false; if (s) return s; }
+        { Mark m(c, 1); if ((s = launch_inject(c, dst, k, pdl))) return s; }
         // swap: dst is now the current level
         if (!virt) { Mark m(c, 2); if ((s = launch_faces(c, dst))) return s; }
         if (c->d.world > 1 && c->peer_mode) {

@@ -379,6 +379,19 @@ __global__ void __launch_bounds__(ZMarchShape<T, BX>::THREADS)
 
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch.  A kernel launched with the programmatic
+// stream-serialisation attribute may start before its predecessor on the
+// stream has finished; pdl_wait() blocks until that predecessor has completed
+// and its writes are visible.  Both are no-ops for an ordinary launch.  Every
+// PDL-aware kernel calls pdl_wait() in every thread before its first read of
+// data the predecessor writes and before any exit, so completion of a kernel
+// still implies completion of everything before it on the stream.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // TMA + mbarrier helpers (inline PTX, sm_90+/sm_100a)
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -455,7 +468,8 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
     unsigned long long* barU = reinterpret_cast<unsigned long long*>(smem + S::BAR_OFF);
     unsigned long long* barP = barU + NU;
 
-    if (a.ctrl->abort) return;
+    // the next kernel (point sources) may launch once our last wave is placed
+    pdl_launch_dependents();
     const int ty = threadIdx.x, tx = threadIdx.y, tid = tx * NTY + ty;
     const int ty0 = blockIdx.x * TYW;
     const int tx0 = blockIdx.y * BX;
@@ -516,6 +530,9 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
         mbar_fence_init();
     }
     __syncthreads();
+    // everything above touches shared memory and setup-time data only
+    pdl_wait();
+    if (a.ctrl->abort) return;
     if (tid == 0) {
         for (int k = 0; k <= R; ++k) issue_u(k);  // planes zs .. zs+R
         issue_p(0);
@@ -2027,15 +2044,19 @@ __global__ void inject_kernel(T* out, const T* __restrict__ c2dt2, const T* __re
                               unsigned long long n_wavelet, int n_tgt, int k, const Ctrl* ctrl,
                               PeerMirror<T> pm) {
     using A = Ar<T, true>;  // the reference's scalar order; never contracted
-    if (ctrl->abort) return;
+    // Under PDL this runs while the sweep's last wave drains: everything but
+    // out[i] is setup-time data (ctrl->step is advanced only between chunks,
+    // by an ordinary launch), so it is loaded before pdl_wait().
+    pdl_launch_dependents();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_tgt) return;
     const unsigned long long n = ctrl->step + (unsigned long long)k;
-    if (n >= n_wavelet) return;
-    const double amp = wavelet[n];
-    const long long i = tgt[t];
-    const T c2 = c2dt2[i];
-    const T e = eta[i];
+    const bool act = t < n_tgt && n < n_wavelet;
+    const double amp = act ? wavelet[n] : 0.0;
+    const long long i = act ? tgt[t] : 0;
+    const T c2 = act ? c2dt2[i] : T(0);
+    const T e = act ? eta[i] : T(0);
+    pdl_wait();
+    if (ctrl->abort || !act) return;
     T om, iop = T(1);
     if (e != T(0)) damping_factors(e, dt, om, iop);
     T val = out[i];
