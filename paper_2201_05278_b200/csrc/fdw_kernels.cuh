@@ -2258,7 +2258,6 @@ __global__ void __launch_bounds__(256) health_scan_ext(const T* __restrict__ u, 
     constexpr int V = 16 / sizeof(T);
     using VT = Vec<T, V>;
     if (honor_abort && ctrl->abort) return;
-    const int nv = (ny + V - 1) / V;
     T m = T(0);
     unsigned long long bad = ~0ull;
     auto visit = [&](T val, int z, int x, int y) {
@@ -2272,24 +2271,33 @@ __global__ void __launch_bounds__(256) health_scan_ext(const T* __restrict__ u, 
             m = av > m ? av : m;
         }
     };
-    // a warp per extended row, lanes over its 16-byte vectors
+    // a warp per extended row, lanes over its 16-byte vectors; each lane
+    // issues up to NB independent loads before visiting any of them
+    constexpr int NB = 8;
     const int lane0 = threadIdx.x & 31;
     const int nrows = nz * nx;
+    const int nfull = ny / V;  // whole vectors; the ragged tail is visited scalar
     for (int row = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); row < nrows;
          row += (int)((gridDim.x * blockDim.x) >> 5)) {
         const int z = row / nx, x = row - z * nx;
         const T* p = u + origin + (long long)z * plane + (long long)x * ld;
-#pragma unroll 4
-        for (int v = lane0; v < nv; v += 32) {
-            const int y0 = v * V;
-            if (y0 + V <= ny) {
-                const VT t = ldg16(p + y0);
+        for (int b = 0; b < nfull; b += 32 * NB) {
+            VT t[NB];
 #pragma unroll
-                for (int e = 0; e < V; ++e) visit(t.e[e], z, x, y0 + e);
-            } else {
-                for (int e = 0; y0 + e < ny; ++e) visit(p[y0 + e], z, x, y0 + e);
+            for (int j = 0; j < NB; ++j) {
+                const int v = b + j * 32 + lane0;
+                if (v < nfull) t[j] = ldg16(p + v * V);
+            }
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                const int v = b + j * 32 + lane0;
+                if (v < nfull) {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) visit(t[j].e[e], z, x, v * V + e);
+                }
             }
         }
+        for (int y = nfull * V + lane0; y < ny; y += 32) visit(p[y], z, x, y);
     }
     double md = static_cast<double>(m);
     for (int o = 16; o > 0; o >>= 1) {
