@@ -1477,7 +1477,7 @@ fdw_status enqueue_split_sweep_t(fdw_solver* c, int k, int src, int dst) {
 
 bool use_pdl(const fdw_solver* c) {
     static const bool off = std::getenv("FDW_NO_PDL") != nullptr;
-    return !off && c->variant == FDW_KERNEL_TMA && !c->vd && c->d.world == 1 && !c->prof && c->vs_fields.empty();
+    return !off && c->variant == FDW_KERNEL_TMA && c->d.world == 1 && !c->prof && c->vs_fields.empty();
 }
 
 fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
