@@ -6,11 +6,18 @@ One bench "step" = one complete forward propagation of the workload from the
 quiescent state (Solver<T>::forward, kernel.hpp:237-263): source injection,
 receiver sampling every time step and health checks included.
   N = 1 : C4, 3D Overthrust-shaped 217x811x811 extended grid, SO=8, 2650 steps.
-  N > 1 : weak scaling -- one C4-sized slab (217 extended Z planes) per GPU,
-          Z-slab decomposition with an R-plane NCCL halo exchange every step.
+  N > 1 : C5 weak scaling (BASELINE config 5) -- 200 extended Z planes x 811 x
+          811 per GPU, SO=8, 500 steps; --workload C4 is the strong-scaling
+          split of C4 (BASELINE config 4: slabs 109/108, 55/54, 28/27).
+          Z slabs; each step's sweep stores its R boundary planes straight
+          into the neighbours' ghost planes over NVLink peer memory.  Before
+          timing, a reduced grid over the same ranks is checked bit for bit
+          against one domain ("parity" in the line).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-Launched with torchrun for N > 1 (one rank per GPU, RANK/LOCAL_RANK/WORLD_SIZE).
+                  [--workload auto|C1..C5|C4w] [--devices 0,1,...]
+N > 1 runs under torchrun (one process per GPU, RANK/LOCAL_RANK/WORLD_SIZE) or,
+launched directly, as one process with a host thread per GPU.
 Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
@@ -41,7 +48,10 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--workload", default="auto", help="auto | C1 | C2 | C3 | C4")
+    p.add_argument("--workload", default="auto", help="auto | C1 | C2 | C3 | C4 | C5 | C4w")
+    p.add_argument("--devices", default="", help="N > 1 without torchrun: CUDA ordinals, one per rank "
+                                                  "(default 0..N-1; repeated ordinals = host-ordered emulation)")
+    p.add_argument("--no-parity", action="store_true")
     p.add_argument("--math", default="exact", choices=["exact", "fma"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
@@ -59,11 +69,16 @@ def peaks():
 
 
 def workload_cfg(name, world):
+    """auto: C4 on one GPU, C5 (weak scaling, 200 planes per GPU) on N > 1.
+    C3 / C4 on N > 1 are strong scaling (the one grid split into N slabs);
+    C4w is weak scaling with one C4-sized slab (217 planes) per GPU."""
     from paper_2201_05278_b200 import configs
     if name == "auto":
-        name = "C4"
-    if name == "C4" and world > 1:
-        return "C4w", configs.overthrust3d(8, z_planes_ext=217 * world)
+        name = "C4" if world == 1 else "C5"
+    if name == "C5":
+        return name, configs.weak3d(world)
+    if name == "C4w":
+        return name, configs.overthrust3d(8, z_planes_ext=217 * world)
     return name, configs.CONFIGS[name]()
 
 
@@ -80,6 +95,8 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        if self.dev is None:  # ranks other than 0 do not sample
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -128,60 +145,236 @@ def traffic_for(workload):
 
 
 # --------------------------------------------------------------------------
+class TorchEnv:
+    """One process per GPU under torchrun (RANK / LOCAL_RANK / WORLD_SIZE):
+    torch.distributed carries only control traffic; the ranks' levels and
+    sync blocks are IPC-mapped (dist.link_peers)."""
+
+    def __init__(self, world, rank, local):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.world, self.rank, self.device = world, rank, local
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        self.transport = "peer: NVLink P2P stores from the sweep into IPC-mapped neighbour levels, halo epochs"
+
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        self.dist.barrier()
+        self.torch.cuda.synchronize()
+
+    def gather(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def allmax(self, x):
+        return max(self.gather(float(x)))
+
+    def link(self, solver):
+        from paper_2201_05278_b200 import dist as fdist
+        fdist.link_peers(solver)
+
+    def close(self):
+        self.dist.barrier()
+        self.dist.destroy_process_group()
+
+
+class ThreadShared:
+    def __init__(self, devices):
+        self.devices = list(devices)
+        self.world = len(self.devices)
+        self.bar = threading.Barrier(self.world, timeout=1800)
+        self.slots = [None] * self.world
+
+
+class ThreadEnv:
+    """One process driving N GPUs, one host thread per rank (no torchrun):
+    the slab Solvers are linked in-process (fdw_peer_link).  Ranks that share
+    a GPU (--devices 0,0: emulation) run host-ordered."""
+
+    def __init__(self, shared, rank):
+        import torch
+        self.torch, self.sh = torch, shared
+        self.world, self.rank, self.device = shared.world, rank, shared.devices[rank]
+        torch.cuda.set_device(self.device)
+        shared_gpu = len(set(shared.devices)) < shared.world
+        self.transport = ("host-ordered peer stores (ranks share a GPU: emulation, not a scaling number)"
+                          if shared_gpu else
+                          "peer: NVLink P2P stores from the sweep into the neighbours' levels, halo epochs "
+                          "(one process, a thread per GPU)")
+
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        self.sh.bar.wait()
+
+    def gather(self, obj):
+        self.sh.slots[self.rank] = obj
+        self.sh.bar.wait()
+        out = list(self.sh.slots)
+        self.sh.bar.wait()
+        return out
+
+    def allmax(self, x):
+        return max(self.gather(float(x)))
+
+    def link(self, solver):
+        solver.peer_link(self.gather(solver))
+
+    def close(self):
+        self.sh.bar.wait()
+
+
+class SoloEnv:
+    world, rank, transport = 1, 0, None
+
+    def __init__(self, device=0):
+        import torch
+        self.torch, self.device = torch, device
+        torch.cuda.set_device(device)
+
+    def barrier(self):
+        self.torch.cuda.synchronize()
+
+    def gather(self, obj):
+        return [obj]
+
+    def allmax(self, x):
+        return float(x)
+
+    def link(self, solver):
+        pass
+
+    def close(self):
+        pass
+
+
+def parity_check(env, math_mode):
+    """N > 1 self-check before timing: a reduced grid decomposed over the same
+    ranks as the timed run (same kernels, same peer transport, a point source
+    whose taps straddle a slab face), started from a random state so that
+    every halo exchange matters from the first step, compared with the same
+    grid as one domain on rank 0's GPU.  Field: bit for bit; seismogram: the
+    rank-ordered sum of double partials within 1e-12 (relative L2)."""
+    from paper_2201_05278_b200 import DampingField, Solver, make_material_model
+    from paper_2201_05278_b200.configs import SyntheticConfig, build_workload
+    world, rank = env.world, env.rank
+    per, h = 24, 20.0
+    nz_int = per * world - 10
+    z_face = h * (per - 5) + h / 2  # extended plane 24.5: taps on both sides of the first slab face
+    cfg = SyntheticConfig(
+        name=f"parity-p{world}", ndim=3, bbox=[0.0, h * (nz_int - 1), 0.0, h * 120, 0.0, h * 120],
+        spacing=[h, h, h], space_order=8, damping=[100.0] * 6, vmin=2000.0, vmax=6000.0, tf=0.0,
+        sources=[(z_face, h * 60.5, h * 60.5), (h * (per * world - 14) + h / 2, h * 30.5, h * 80.5)],
+        receivers=[(h * (per - 6) + h / 2, h * (3 + k), h * 60.5) for k in range(100)], fixed_steps=24)
+    w = build_workload(cfg, np.float32, rank=rank, world=world)
+    R = w.grid.halo
+    P = w.grid.padded_shape()
+    rng = np.random.default_rng(2201)
+    prev = (rng.standard_normal(P) * 1e-3).astype(np.float32)
+    curr = (rng.standard_normal(P) * 1e-3).astype(np.float32)
+    zb, ze = w.slab[2], w.slab[3]
+    s = Solver(w.grid, make_material_model(w.velocity), DampingField(eta=w.eta), w.spec, w.axis, w.coeffs,
+               device=env.device, math=math_mode, slab=w.slab)
+    env.link(s)
+    s.set_sources(w.sources, w.wavelet)
+    s.set_receivers(w.receivers)
+    s.previous_level()[...] = prev[zb:ze + 2 * R]
+    s.current_level()[...] = curr[zb:ze + 2 * R]
+    s.refresh_boundary()
+    from paper_2201_05278_b200._lib import lib
+    lib().fdw_record(s.ctx)
+    s.advance_raw(w.axis.n_steps, record=True)
+    parts = env.gather((s.extended_level(), s.seismogram_f64()))
+    s.close()
+    if rank != 0:
+        env.barrier()
+        return None
+    wf = build_workload(cfg, np.float32)
+    r = Solver(wf.grid, make_material_model(wf.velocity), DampingField(eta=wf.eta), wf.spec, wf.axis, wf.coeffs,
+               device=env.device, math=math_mode)
+    r.set_sources(wf.sources, wf.wavelet)
+    r.set_receivers(wf.receivers)
+    r.previous_level()[...] = prev
+    r.current_level()[...] = curr
+    r.refresh_boundary()
+    lib().fdw_record(r.ctx)
+    r.advance_raw(wf.axis.n_steps, record=True)
+    ref_field, ref_seis = r.extended_level(), r.seismogram_f64()
+    r.close()
+    env.barrier()
+    field = np.concatenate([p[0] for p in parts], axis=0)
+    seis = parts[0][1].copy()
+    for p in parts[1:]:
+        seis += p[1]
+    rel = float(np.linalg.norm(seis - ref_seis) / max(np.linalg.norm(ref_seis), 1e-300))
+    exact = bool(np.array_equal(field, ref_field))
+    return {"ok": bool(exact and rel <= 1e-12 and np.abs(ref_field).max() > 0), "field_bit_exact": exact,
+            "seismogram_rel_l2": rel, "case": f"{cfg.name}: {world} slabs of {per} planes x 131 x 131, SO8, "
+                                                f"random start, 24 steps vs one domain on rank 0's GPU"}
+
+
 def run_ours(args):
+    """Dispatch: N = 1 (one GPU), torchrun (one process per GPU), or one
+    process with a thread per GPU when --gpus N > 1 is launched directly."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        if world != args.gpus:
+            raise SystemExit(f"WORLD_SIZE {world} != --gpus {args.gpus}")
+        env = TorchEnv(world, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")))
+        return bench_rank(args, env)
+    if args.gpus <= 1:
+        return bench_rank(args, SoloEnv(int(args.devices.split(",")[0]) if args.devices else 0))
+    devices = [int(x) for x in args.devices.split(",")] if args.devices else list(range(args.gpus))
+    if len(devices) != args.gpus:
+        raise SystemExit("--devices must list --gpus ordinals")
+    sh = ThreadShared(devices)
+    out, errs = [None] * args.gpus, []
+
+    def go(r):
+        try:
+            out[r] = bench_rank(args, ThreadEnv(sh, r))
+        except BaseException as e:  # surfaced below; unblock the other ranks
+            import traceback
+            errs.append(f"rank {r}: {traceback.format_exc()}")
+            sh.bar.abort()
+
+    th = [threading.Thread(target=go, args=(r,), daemon=True) for r in range(args.gpus)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise SystemExit("\n".join(errs))
+    return out[0]
+
+
+def bench_rank(args, env):
     import torch
-    import torch.distributed as dist
 
     from paper_2201_05278_b200 import DampingField, Solver, make_material_model
     from paper_2201_05278_b200._lib import FDW_MATH_EXACT, FDW_MATH_FMA, lib
     from paper_2201_05278_b200.configs import build_workload
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N > 1 must be launched with torchrun (one rank per GPU)")
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world, rank, dev = env.world, env.rank, env.device
     wname, cfg = workload_cfg(args.workload, world)
     math_mode = FDW_MATH_EXACT if args.math == "exact" else FDW_MATH_FMA
+    parity = parity_check(env, math_mode) if world > 1 and not args.no_parity else None
 
     t0 = time.time()
     w = build_workload(cfg, np.float32, rank=rank, world=world)
     setup_s = time.time() - t0
-    slab = None
-    # halo transport for N > 1: "peer" (default; the sweep stores the halo
-    # planes straight into the neighbours' levels over NVLink) or "nccl"
-    halo = os.environ.get("FDW_HALO", "peer")
-    if world > 1 and halo == "nccl":
-        import ctypes as C
-        idbuf = (C.c_ubyte * 128)()
-        if rank == 0:
-            lib().fdw_nccl_unique_id(C.byref(idbuf))
-        obj = [bytes(idbuf)]
-        dist.broadcast_object_list(obj, src=0)
-        slab = (*w.slab, obj[0])
-    elif world > 1:
-        slab = (*w.slab, None)
-    stream = torch.cuda.Stream()
+    slab = w.slab if world > 1 else None
+    stream = torch.cuda.Stream(device=dev)
 
     def make_solver(vel, eta, mats=None):
-        t0 = time.perf_counter()
         s = Solver(w.grid, mats or make_material_model(vel), DampingField(eta=eta), w.spec, w.axis, w.coeffs,
-                   device=local, math=math_mode, slab=slab)
-        t1 = time.perf_counter()
+                   device=dev, math=math_mode, slab=slab)
         s.set_stream(stream.cuda_stream)
-        if world > 1 and halo != "nccl":
-            from paper_2201_05278_b200 import dist as fdist
-            fdist.link_peers(s)
-        t2 = time.perf_counter()
+        env.link(s)
         s.set_sources(w.sources, w.wavelet)
         s.set_receivers(w.receivers)
-        if os.environ.get("FDW_BENCH_DEBUG"):
-            print(f"  make_solver: Solver() {t1 - t0:.3f}, set_stream {t2 - t1:.3f}, maps "
-                  f"{time.perf_counter() - t2:.3f}", file=sys.stderr, flush=True)
         return s
 
     solver = make_solver(w.velocity, w.eta)
@@ -195,30 +388,20 @@ def run_ours(args):
         lib().fdw_record(solver.ctx)
         solver.advance_raw(n_steps, record=True)
 
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-            torch.cuda.synchronize()
-
     for _ in range(args.warmup):
         one_forward()
-    barrier()
+    env.barrier()
     l0 = solver.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
+    with ClockSampler(dev if rank == 0 else None) as clk:
+        env.barrier()
         ev0.record(stream)
         for _ in range(args.steps):
             one_forward()
         ev1.record(stream)
-        barrier()
+        env.barrier()
     launches = solver.launch_count() - l0
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = env.allmax(ev0.elapsed_time(ev1))  # device time, max over ranks
     ms_per_step = ms / args.steps
     value = total_pts * n_steps / (ms_per_step * 1e-3) / 1e9
 
@@ -260,7 +443,7 @@ def run_ours(args):
 
         e2e_times = []
         for it in range(max(1, args.steps) + 1):
-            barrier()
+            env.barrier()
             e0 = time.perf_counter()
             s = make_solver(vel_h, eta_h, mats)
             e1 = time.perf_counter()
@@ -269,40 +452,37 @@ def run_ours(args):
             _ = r.seismogram.data, r.snapshots[-1]
             e2 = time.perf_counter()
             s.close()
-            barrier()
+            env.barrier()
             el = time.perf_counter() - e0
             if os.environ.get("FDW_BENCH_DEBUG"):
                 print(f"e2e iter {it}: {el:.3f} s (ctor {e1 - e0:.3f}, forward {e2 - e1:.3f}, kernel "
                       f"{r.kernel_seconds:.3f}, close {el - (e2 - e0):.3f})", file=sys.stderr, flush=True)
             if it > 0:  # first call pays graph capture
                 e2e_times.append(el)
-        el = statistics.mean(e2e_times)
-        if world > 1:
-            t = torch.tensor([el], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        el = env.allmax(statistics.mean(e2e_times))
         e2e = {"value": round(total_pts * n_steps / el / 1e9, 3), "unit": UNIT,
                "h2d_bytes_per_step": int(vel_h.nbytes + eta_h.nbytes + w.sources.weight.nbytes * 2
                                          + w.receivers.weight.nbytes * 2 + w.wavelet.nbytes),
                "d2h_bytes_per_step": int(seis_bytes + ext_bytes),
                "api": "paper_2201_05278_b200.Solver(...) + set_sources/receivers + forward() over "
                       "libfdwave_cuda.so; pinned host buffers; velocity/eta H2D, seismogram + final "
-                      "snapshot D2H inside the timed region",
+                      "snapshot D2H inside the timed region" + (" (per rank: its slab)" if world > 1 else ""),
                "seconds_per_step": round(el, 4)}
+    else:
+        solver.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(cfg, args.cpu_seconds)
 
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    env.close()
     if rank != 0:
         return None
+    strong = world > 1 and wname in ("C3", "C4")
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": round(value / BASELINE_GPTS["C4"], 2) if wname in BASELINE_GPTS else None,
         "dtype": "f32", "data": "synthetic",
         "config": {
@@ -310,7 +490,7 @@ def run_ours(args):
             "space_order": cfg.space_order, "time_steps": n_steps, "points_per_gpu": local_pts,
             "total_points": total_pts, "receivers": w.receivers.n_points, "sources": w.sources.n_points,
             "math": args.math,
-            "parallelism": f"z-slab x{world} ({halo} halo)" if world > 1 else "single GPU",
+            "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
             "step": "one full forward propagation from rest (inject + record every time step, health every 100)",
             "l2": "inputs exceed L2 (4 fields x ~0.7 GB >> 126 MB); no flush needed",
             "setup_seconds": round(setup_s, 2),
@@ -330,6 +510,9 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if world > 1:
+        line["transport"] = env.transport
+        line["parity"] = parity
     return line
 
 

@@ -24,15 +24,19 @@
 // :439-452).  set_backend is accepted and ignored.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <chrono>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <exception>
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <utility>
 #include <vector>
@@ -180,7 +184,67 @@ struct ForwardResult {
 
 enum class Backend { Serial, Parallel };
 
-/// fdwave::Solver<T> on a B200 through libfdwave_cuda.so.
+namespace detail {
+
+/// FDW_DEVICES: the GPUs one Solver spreads a 3D grid over as Z slabs, e.g.
+/// "0-7" or "0,1,2,3" (repeated ordinals emulate slabs on one GPU; the
+/// library then orders the ranks on the host).  Unset: device 0 only.
+inline std::vector<int> devices_from_env() {
+    std::vector<int> out;
+    const char* env = std::getenv("FDW_DEVICES");
+    if (!env || !*env) return out;
+    std::string spec(env);
+    std::size_t pos = 0;
+    while (pos <= spec.size()) {
+        const std::size_t comma = spec.find(',', pos);
+        const std::string tok = spec.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+        const std::size_t dash = tok.find('-');
+        if (!tok.empty()) {
+            if (dash != std::string::npos) {
+                const int lo = std::stoi(tok.substr(0, dash)), hi = std::stoi(tok.substr(dash + 1));
+                for (int d = lo; d <= hi; ++d) out.push_back(d);
+            } else {
+                out.push_back(std::stoi(tok));
+            }
+        }
+        if (comma == std::string::npos) break;
+        pos = comma + 1;
+    }
+    return out;
+}
+
+/// Runs f(r) for every rank concurrently (one host thread each: the ranks of
+/// a slab decomposition wait on each other inside collective calls) and
+/// rethrows the first failure.
+template <class F>
+void on_ranks(std::size_t n, F&& f) {
+    if (n == 1) {
+        f(std::size_t(0));
+        return;
+    }
+    std::vector<std::exception_ptr> err(n);
+    std::vector<std::thread> th;
+    th.reserve(n);
+    for (std::size_t r = 0; r < n; ++r)
+        th.emplace_back([&, r] {
+            try {
+                f(r);
+            } catch (...) {
+                err[r] = std::current_exception();
+            }
+        });
+    for (auto& t : th) t.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
+
+}  // namespace detail
+
+/// fdwave::Solver<T> on a B200 through libfdwave_cuda.so.  With FDW_DEVICES
+/// naming several GPUs, a 3D Solver is one Z slab per GPU (the reference's
+/// OpenMP loop over Z planes, kernel.hpp:392-393, becomes a loop over GPUs):
+/// the slabs exchange their halo planes over NVLink peer memory inside each
+/// step, and this class scatters / gathers the host-side views.
 template <typename T>
 class Solver {
     static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>,
@@ -192,6 +256,11 @@ public:
         : grid_(std::move(grid)), boundary_(boundary), time_(time), coeffs_(std::move(coeffs)) {
         if (coeffs_.order != grid_.space_order)
             throw std::invalid_argument("stencil order does not match grid order");
+        std::vector<int> devs = detail::devices_from_env();
+        if (devs.empty()) devs.push_back(0);
+        if (grid_.ndim != 3 || devs.size() > grid_.extended_shape[0] / (2 * std::size_t(grid_.halo)))
+            devs.resize(1);  // 2D, or slabs thinner than 2R planes: one GPU
+        const std::size_t world = devs.size();
         fdw_desc d;
         fdw_desc_init(&d);
         d.ndim = grid_.ndim;
@@ -206,18 +275,45 @@ public:
         for (std::size_t j = 0; j < coeffs_.first.size() && j < 10; ++j) d.coeffs1[j] = coeffs_.first[j];
         d.dt = time_.dt;
         d.n_steps = time_.n_steps;
-        check(fdw_create(&d, &ctx_), "fdw_create", true);
+        const auto pad = grid_.padded_shape();
+        plane_ = pad[1] * pad[2];
+        ctxs_.assign(world, nullptr);
+        slabs_.assign(world, {0, grid_.extended_shape[0]});
         try {
-            check(fdw_set_medium(ctx_, materials.velocity.data(), damping.eta.data(), 0), "fdw_set_medium");
-            if (materials.density) {
-                if (materials.density->size() != materials.velocity.size())
-                    throw std::invalid_argument("material model: density shape mismatch");
-                check(fdw_set_density(ctx_, materials.density->data(), 0), "fdw_set_density");
+            for (std::size_t r = 0; r < world; ++r) {
+                fdw_desc dr = d;
+                dr.device = devs[r];
+                if (world > 1) {
+                    uint64_t zb = 0, ze = 0;
+                    check_ctx(fdw_slab_range(grid_.extended_shape[0], static_cast<int32_t>(world),
+                                             static_cast<int32_t>(r), &zb, &ze),
+                              nullptr, "fdw_slab_range");
+                    dr.rank = static_cast<int32_t>(r);
+                    dr.world = static_cast<int32_t>(world);
+                    dr.z_begin = zb;
+                    dr.z_end = ze;
+                    slabs_[r] = {zb, ze};
+                }
+                check_ctx(fdw_create(&dr, &ctxs_[r]), nullptr, "fdw_create");
+                const std::size_t off = slabs_[r].first * plane_;  // local padded slab = contiguous planes
+                check_ctx(fdw_set_medium(ctxs_[r], materials.velocity.data() + off, damping.eta.data() + off, 0),
+                          ctxs_[r], "fdw_set_medium");
+                if (materials.density) {
+                    if (materials.density->size() != materials.velocity.size())
+                        throw std::invalid_argument("material model: density shape mismatch");
+                    check_ctx(fdw_set_density(ctxs_[r], materials.density->data() + off, 0), ctxs_[r],
+                              "fdw_set_density");
+                }
             }
+            if (world > 1)
+                for (std::size_t r = 0; r < world; ++r)
+                    check_ctx(fdw_peer_link(ctxs_[r], ctxs_.data(), static_cast<int32_t>(world)), ctxs_[r],
+                              "fdw_peer_link");
         } catch (...) {
             release();
             throw;
         }
+        ctx_ = ctxs_[0];
         prev_ = Field<T>(grid_.ndim, grid_.padded_shape());
         curr_ = Field<T>(grid_.ndim, grid_.padded_shape());
     }
@@ -239,12 +335,20 @@ public:
             verbose_ = o.verbose_;
             snapshot_cap_bytes_ = o.snapshot_cap_bytes_;
             mirrored_ = o.mirrored_;
+            loop_start_ = o.loop_start_;
+            plane_ = o.plane_;
+            ctxs_ = std::move(o.ctxs_);
+            slabs_ = std::move(o.slabs_);
             ctx_ = o.ctx_;
             o.ctx_ = nullptr;
+            o.ctxs_.clear();
         }
         return *this;
     }
     ~Solver() { release(); }
+
+    /// Number of GPUs (Z slabs) this Solver runs on.
+    std::size_t devices() const { return ctxs_.size(); }
 
     void set_sources(InterpolationMap sources, std::vector<double> wavelet) {
         if (!sources.points.empty() && wavelet.size() < time_.sample_count())
@@ -252,16 +356,18 @@ public:
         std::vector<uint64_t> off, idx;
         std::vector<double> w;
         flatten(sources, off, idx, w);
-        check(fdw_set_sources(ctx_, sources.points.size(), off.data(), idx.data(), w.data(), wavelet.data(),
-                              wavelet.size()),
-              "fdw_set_sources");
+        for (auto* c : ctxs_)  // each slab keeps the taps it owns
+            check_ctx(fdw_set_sources(c, sources.points.size(), off.data(), idx.data(), w.data(), wavelet.data(),
+                                      wavelet.size()),
+                      c, "fdw_set_sources");
     }
     void set_receivers(InterpolationMap receivers, std::vector<std::array<double, 3>> coordinates = {}) {
         std::vector<uint64_t> off, idx;
         std::vector<double> w;
         flatten(receivers, off, idx, w);
-        check(fdw_set_receivers(ctx_, receivers.points.size(), off.data(), idx.data(), w.data()),
-              "fdw_set_receivers");
+        for (auto* c : ctxs_)
+            check_ctx(fdw_set_receivers(c, receivers.points.size(), off.data(), idx.data(), w.data()), c,
+                      "fdw_set_receivers");
         n_receivers_ = receivers.points.size();
         receiver_coordinates_ = std::move(coordinates);
     }
@@ -271,8 +377,10 @@ public:
         const auto pad = grid_.padded_shape();
         if (source.field.size() != pad[0] * pad[1] * pad[2])
             throw std::invalid_argument("volume source field shape mismatch");
-        check(fdw_add_volume_source(ctx_, source.field.data(), source.amplitude.data(), source.amplitude.size(), 0),
-              "fdw_add_volume_source");
+        for (std::size_t r = 0; r < ctxs_.size(); ++r)
+            check_ctx(fdw_add_volume_source(ctxs_[r], source.field.data() + slabs_[r].first * plane_,
+                                            source.amplitude.data(), source.amplitude.size(), 0),
+                      ctxs_[r], "fdw_add_volume_source");
     }
     void set_backend(Backend, int) {}
     void set_verbose(bool verbose) { verbose_ = verbose; }
@@ -296,7 +404,8 @@ public:
 
     void refresh_boundary() {
         push();
-        check(fdw_refresh_boundary(ctx_), "fdw_refresh_boundary");
+        detail::on_ranks(ctxs_.size(),
+                         [&](std::size_t r) { check_ctx(fdw_refresh_boundary(ctxs_[r]), ctxs_[r], "fdw_refresh_boundary"); });
         pull();
     }
 
@@ -317,11 +426,12 @@ public:
         // snapshot buffers are written asynchronously: keep them in place
         result.snapshots.reserve(time_.snapshot_count() + 1);
         refresh_boundary();
-        check(fdw_record(ctx_), "fdw_record");
+        for (auto* c : ctxs_) check_ctx(fdw_record(c), c, "fdw_record");
         const std::size_t start = step_index(), n = time_.n_steps, stride = time_.saving_stride;
         auto due = [&](std::size_t s) { return stride == 0 ? s == n : s % stride == 0; };
         if (due(start)) snapshot(result, start);
         const auto t0 = std::chrono::steady_clock::now();
+        loop_start_ = t0;
         std::size_t cur = start;
         const std::size_t end = start + n;
         // steps and snapshot copies are queued without host syncs; each
@@ -339,8 +449,19 @@ public:
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (n_receivers_) {
             result.seismogram.data.resize((n + 1) * n_receivers_);
-            check(fdw_download_seismogram(ctx_, result.seismogram.data.data(), n + 1),
-                  "fdw_download_seismogram");
+            if (ctxs_.size() == 1) {
+                check(fdw_download_seismogram(ctx_, result.seismogram.data.data(), n + 1),
+                      "fdw_download_seismogram");
+            } else {
+                // per-slab double partial sums, added in rank order, cast to T
+                // (acquisition.hpp:155-158 split at the slab faces)
+                std::vector<double> acc((n + 1) * n_receivers_, 0.0), part(acc.size());
+                for (auto* c : ctxs_) {
+                    check_ctx(fdw_download_seismogram_f64(c, part.data(), n + 1), c, "fdw_download_seismogram");
+                    for (std::size_t i = 0; i < acc.size(); ++i) acc[i] += part[i];
+                }
+                for (std::size_t i = 0; i < acc.size(); ++i) result.seismogram.data[i] = static_cast<T>(acc[i]);
+            }
         }
         pull();
         return result;
@@ -348,9 +469,10 @@ public:
 
     double max_abs() const {
         const_cast<Solver*>(this)->push();
-        double m = 0.0;
-        check(fdw_max_abs(ctx_, &m), "fdw_max_abs");
-        return m;
+        std::vector<double> m(ctxs_.size(), 0.0);
+        detail::on_ranks(ctxs_.size(),
+                         [&](std::size_t r) { check_ctx(fdw_max_abs(ctxs_[r], &m[r]), ctxs_[r], "fdw_max_abs"); });
+        return m[0];  // reduced over every slab
     }
 
 private:
@@ -370,62 +492,131 @@ private:
         }
     }
 
-    void check(fdw_status s, const char* what, bool creating = false) const {
+    static void check_ctx(fdw_status s, const fdw_solver* c, const char* what) {
         if (s == FDW_OK) return;
-        const std::string msg = std::string(what) + ": " + fdw_last_error(creating ? nullptr : ctx_);
+        const std::string msg = std::string(what) + ": " + fdw_last_error(c);
         if (s == FDW_EINVAL) throw std::invalid_argument(msg);
         throw std::runtime_error(msg);
     }
+    void check(fdw_status s, const char* what) const { check_ctx(s, ctx_, what); }
+
+    // fdw_advance on every slab; an instability (the same step on every rank:
+    // the health check is reduced across slabs) becomes instability_error
+    void advance_ranks(std::size_t n, uint32_t flags) {
+        std::vector<uint64_t> bad_step(ctxs_.size(), 0);
+        std::vector<double> bad_max(ctxs_.size(), 0.0);
+        std::vector<fdw_status> st(ctxs_.size(), FDW_OK);
+        detail::on_ranks(ctxs_.size(), [&](std::size_t r) {
+            st[r] = fdw_advance(ctxs_[r], n, flags, &bad_step[r], &bad_max[r]);
+        });
+        for (std::size_t r = 0; r < ctxs_.size(); ++r)
+            if (st[r] == FDW_EINSTABLE) {
+                pull();
+                throw instability_error(bad_step[r], bad_max[r]);
+            }
+        for (std::size_t r = 0; r < ctxs_.size(); ++r) check_ctx(st[r], ctxs_[r], "fdw_advance");
+    }
 
     void advance(std::size_t n, uint32_t flags) {
-        uint64_t bad_step = 0;
-        double bad_max = 0.0;
-        const fdw_status s = fdw_advance(ctx_, n, flags, &bad_step, &bad_max);
-        if (s == FDW_EINSTABLE) {
-            pull();
-            throw instability_error(bad_step, bad_max);
+        if (verbose_) {  // the reference's progress line at every health check
+            verbose_advance(n, flags & ~uint32_t(FDW_ADVANCE_ASYNC));
+            return;
         }
-        check(s, "fdw_advance");
-        if (verbose_)
-            std::fprintf(stderr, "step %zu/%zu\n", step_index(), static_cast<std::size_t>(time_.n_steps));
+        advance_ranks(n, flags);
+    }
+
+    // check_health's verbose branch (kernel.hpp:456-466): the steps run in
+    // pieces that end at the health checks (step % 100 == 0 or the last
+    // step); after each, the line "step s/N  t s  max|p| = m" with the time
+    // since forward() started its loop (or since construction, as there).
+    void verbose_advance(std::size_t n, uint32_t flags) {
+        const std::size_t ci = 100, total = time_.n_steps;
+        std::size_t s = step_index();
+        const std::size_t end = s + n;
+        while (s < end) {
+            std::size_t next = (s / ci + 1) * ci;
+            if (total > s) next = std::min(next, total);
+            next = std::min(next, end);
+            advance_ranks(next - s, flags);
+            s = next;
+            if (s % ci == 0 || s == total) {
+                std::vector<double> m(ctxs_.size(), 0.0);
+                detail::on_ranks(ctxs_.size(), [&](std::size_t r) {
+                    check_ctx(fdw_max_abs(ctxs_[r], &m[r]), ctxs_[r], "fdw_max_abs");
+                });
+                const double el =
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - loop_start_).count();
+                std::fprintf(stderr, "step %zu/%zu  %.3fs  max|p| = %.6e\n", s, total, el, m[0]);
+            }
+        }
     }
 
     void wait() {
-        uint64_t bad_step = 0;
-        double bad_max = 0.0;
-        const fdw_status st = fdw_wait(ctx_, &bad_step, &bad_max);
-        if (st == FDW_EINSTABLE) {
-            pull();
-            throw instability_error(bad_step, bad_max);
-        }
-        check(st, "fdw_wait");
+        std::vector<uint64_t> bad_step(ctxs_.size(), 0);
+        std::vector<double> bad_max(ctxs_.size(), 0.0);
+        std::vector<fdw_status> st(ctxs_.size(), FDW_OK);
+        for (std::size_t r = 0; r < ctxs_.size(); ++r) st[r] = fdw_wait(ctxs_[r], &bad_step[r], &bad_max[r]);
+        for (std::size_t r = 0; r < ctxs_.size(); ++r)
+            if (st[r] == FDW_EINSTABLE) {
+                pull();
+                throw instability_error(bad_step[r], bad_max[r]);
+            }
+        for (std::size_t r = 0; r < ctxs_.size(); ++r) check_ctx(st[r], ctxs_[r], "fdw_wait");
     }
 
-    void snapshot(ForwardResult<T>& r, std::size_t s, bool stream = false) {
+    void snapshot(ForwardResult<T>& res, std::size_t s, bool stream = false) {
         Field<T> out(grid_.ndim, grid_.extended_shape);
-        if (stream)  // filled by the copy stream; valid after wait()
-            check(fdw_snapshot_async(ctx_, out.data()), "fdw_snapshot_async");
-        else
-            check(fdw_get_extended(ctx_, out.data()), "fdw_get_extended");
-        r.snapshots.push_back(std::move(out));
-        r.snapshot_steps.push_back(s);
+        const std::size_t eplane = grid_.ndim == 3 ? grid_.extended_shape[1] * grid_.extended_shape[2] : 0;
+        for (std::size_t r = 0; r < ctxs_.size(); ++r) {  // each slab fills its own planes
+            T* dst = out.data() + slabs_[r].first * eplane;
+            if (stream)  // filled by the copy stream; valid after wait()
+                check_ctx(fdw_snapshot_async(ctxs_[r], dst), ctxs_[r], "fdw_snapshot_async");
+            else
+                check_ctx(fdw_get_extended(ctxs_[r], dst), ctxs_[r], "fdw_get_extended");
+        }
+        res.snapshots.push_back(std::move(out));
+        res.snapshot_steps.push_back(s);
     }
 
-    // host mirrors: downloaded on first access, then kept coherent
+    // host mirrors: downloaded on first access, then kept coherent.  Slabs:
+    // each rank's owned planes (plus the global Z ghost planes on the first
+    // and last rank) are gathered; uploads hand every rank its padded slab.
+    void gather_levels() {
+        if (ctxs_.size() == 1) {
+            check(fdw_get_levels(ctx_, prev_.data(), curr_.data()), "fdw_get_levels");
+            return;
+        }
+        const std::size_t h = static_cast<std::size_t>(grid_.halo), world = ctxs_.size();
+        detail::on_ranks(world, [&](std::size_t r) {
+            const std::size_t zb = slabs_[r].first, ze = slabs_[r].second, nl = ze - zb + 2 * h;
+            std::vector<T> p(nl * plane_), c(nl * plane_);
+            check_ctx(fdw_get_levels(ctxs_[r], p.data(), c.data()), ctxs_[r], "fdw_get_levels");
+            const std::size_t lo = r == 0 ? 0 : h, hi = r + 1 == world ? nl : nl - h;
+            std::copy(p.begin() + lo * plane_, p.begin() + hi * plane_, prev_.data() + (zb + lo) * plane_);
+            std::copy(c.begin() + lo * plane_, c.begin() + hi * plane_, curr_.data() + (zb + lo) * plane_);
+        });
+    }
     void mirror() {
         if (!mirrored_) {
-            check(fdw_get_levels(ctx_, prev_.data(), curr_.data()), "fdw_get_levels");
+            gather_levels();
             mirrored_ = true;
         }
     }
     void push() {
-        if (mirrored_) check(fdw_set_levels(ctx_, prev_.data(), curr_.data()), "fdw_set_levels");
+        if (!mirrored_) return;
+        for (std::size_t r = 0; r < ctxs_.size(); ++r) {
+            const std::size_t off = slabs_[r].first * plane_;
+            check_ctx(fdw_set_levels(ctxs_[r], prev_.data() + off, curr_.data() + off), ctxs_[r], "fdw_set_levels");
+        }
     }
     void pull() {
-        if (mirrored_) check(fdw_get_levels(ctx_, prev_.data(), curr_.data()), "fdw_get_levels");
+        if (mirrored_) gather_levels();
     }
     void release() {
-        if (ctx_) fdw_destroy(ctx_);
+        for (auto*& c : ctxs_) {
+            if (c) fdw_destroy(c);
+            c = nullptr;
+        }
         ctx_ = nullptr;
     }
 
@@ -439,7 +630,11 @@ private:
     bool verbose_ = false;
     std::size_t snapshot_cap_bytes_ = std::size_t(4) << 30;
     bool mirrored_ = false;
-    fdw_solver* ctx_ = nullptr;
+    std::size_t plane_ = 0;                                    // padded elements per Z plane
+    std::vector<fdw_solver*> ctxs_;                            // one context per GPU (Z slab)
+    std::vector<std::pair<std::size_t, std::size_t>> slabs_;   // owned extended Z planes per rank
+    fdw_solver* ctx_ = nullptr;                                // rank 0
+    std::chrono::steady_clock::time_point loop_start_ = std::chrono::steady_clock::now();
 };
 
 }  // namespace fdwave

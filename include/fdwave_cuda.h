@@ -34,13 +34,13 @@
 extern "C" {
 #endif
 
-#define FDW_ABI_VERSION 2
+#define FDW_ABI_VERSION 3
 
 typedef enum fdw_status {
     FDW_OK = 0,
     FDW_EINVAL = 1,     /* maps to std::invalid_argument */
     FDW_ECUDA = 2,      /* CUDA runtime error -> std::runtime_error */
-    FDW_ENCCL = 3,      /* NCCL error -> std::runtime_error */
+    FDW_EPEER = 3,      /* peer transport: a slab rank failed / timed out -> std::runtime_error */
     FDW_EINSTABLE = 4,  /* non-finite wavefield -> fdwave::instability_error */
     FDW_ENOMEM = 5,
     FDW_ESTATE = 6      /* call order violated (e.g. advance before set_medium) */
@@ -93,8 +93,6 @@ typedef struct fdw_desc {
     int32_t z_segments;      /* ZMARCH: Z segments per column (0 -> auto) */
     uint64_t z_begin;        /* first extended Z plane owned by this rank */
     uint64_t z_end;          /* one past the last owned plane */
-    unsigned char nccl_id[128]; /* ncclUniqueId from fdw_nccl_unique_id (world > 1); all zero:
-                                   peer transport (fdw_peer_import / fdw_peer_link) */
     double coeffs1[10];      /* StencilCoeffs::first, w_1..w_r (variable density) stencil.hpp:96 */
 } fdw_desc;
 
@@ -218,17 +216,31 @@ fdw_status fdw_layout(const fdw_solver* ctx, uint64_t* ld, uint64_t* plane,
                       uint64_t* base, uint64_t* planes, int32_t* variant);
 
 /* ---- peer transport (Z slabs over NVLink / NVSwitch peer memory) ----
- * A slab context (world > 1) created with an all-zero desc.nccl_id uses no
- * NCCL: each step's TMA sweep stores its first / last R owned planes straight
- * into the neighbours' ghost planes through mapped peer memory (the point-source
- * kernel does the same for targets in those planes; other paths copy the planes
- * with a push kernel), then one thread per rank signals a step epoch to its
- * neighbours and waits for theirs (release / acquire at system scope).  The
- * health reduction (kernel.hpp:456-458 across slabs) goes through the same
- * per-rank sync blocks.  Replaces the NCCL send/recv of the halo planes.
+ * Replaces the reference's only parallelism, the OpenMP loop over Z planes
+ * (kernel.hpp:392-393), with one GPU per Z slab.  A slab context (world > 1)
+ * exchanges no messages: each step's TMA sweep stores its first / last R owned
+ * planes straight into the neighbours' ghost planes through mapped peer memory
+ * (the point-source kernel does the same for targets in those planes; other
+ * paths copy the planes with a push kernel).  Ordering is one halo epoch per
+ * collective operation: the sweep's boundary CTAs wait until both neighbours
+ * have published this rank's epoch, and the last of them publishes the next
+ * one (release / acquire at system scope).  The health reduction
+ * (kernel.hpp:456-458 across slabs) goes through the same per-rank sync blocks.
  * Every collective call (advance, refresh_boundary, max_abs) must be made on
- * all ranks, as with NCCL; a neighbour that does not signal within 20 s turns
- * into FDW_ECUDA instead of a hang. */
+ * all ranks.  A rank that fails or does not signal within 20 s raises a sticky
+ * abort word in every rank's sync block: every rank then returns FDW_EPEER
+ * instead of hanging or stepping on stale ghost planes.
+ *
+ * Ranks linked in ONE process whose GPUs coincide (one GPU emulating several
+ * slabs) are host-ordered: at each cross-rank point the rank threads meet at a
+ * host barrier and order their streams with events, so no kernel ever waits
+ * on a flag that another launch on the same GPU sets (they run as direct
+ * launches instead of graphs).  IPC-imported neighbours on the same GPU are
+ * refused at the first collective call (FDW_ESTATE).
+ *
+ * Teardown: fdw_destroy waits (bounded) until the neighbours have finished the
+ * epochs this rank went through before it frees the mapped memory; callers
+ * should still destroy all ranks after the same collective calls. */
 #define FDW_PEER_BLOB_BYTES 512
 /* IPC handles of this rank's levels and sync block plus its slab geometry. */
 fdw_status fdw_peer_export(fdw_solver* ctx, unsigned char out[FDW_PEER_BLOB_BYTES]);
@@ -246,8 +258,6 @@ fdw_status fdw_slab_range(uint64_t n_ext, int32_t world, int32_t rank, uint64_t*
 /* Owner rank of global padded flat index (3D slabs; -1 if not an extended point). */
 int32_t fdw_owner_of(uint64_t flat_idx, const uint64_t extended[3], int32_t halo,
                      int32_t world);
-/* ncclGetUniqueId into out[128]. */
-fdw_status fdw_nccl_unique_id(unsigned char out[128]);
 
 #ifdef __cplusplus
 }

@@ -12,8 +12,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FDW_LIB") or os.path.join(_HERE, "libfdwave_cuda.so")  # FDW_LIB: A/B builds
 
-FDW_ABI_VERSION = 2
-FDW_OK, FDW_EINVAL, FDW_ECUDA, FDW_ENCCL, FDW_EINSTABLE, FDW_ENOMEM, FDW_ESTATE = range(7)
+FDW_ABI_VERSION = 3
+FDW_OK, FDW_EINVAL, FDW_ECUDA, FDW_EPEER, FDW_EINSTABLE, FDW_ENOMEM, FDW_ESTATE = range(7)
 FDW_KERNEL_AUTO, FDW_KERNEL_SIMPLE, FDW_KERNEL_ZMARCH, FDW_KERNEL_TMA, FDW_KERNEL_FUSED2D = 0, 1, 2, 3, 4
 FDW_MATH_EXACT, FDW_MATH_FMA = 0, 1
 FDW_ADVANCE_RECORD = 1
@@ -41,7 +41,6 @@ class fdw_desc(C.Structure):
         ("z_segments", C.c_int32),
         ("z_begin", C.c_uint64),
         ("z_end", C.c_uint64),
-        ("nccl_id", C.c_ubyte * 128),
         ("coeffs1", C.c_double * 10),
     ]
 
@@ -83,7 +82,6 @@ _SIGS = {
     "fdw_layout": (C.c_int, [_P, _U64P, _U64P, _U64P, _U64P, C.POINTER(C.c_int32)]),
     "fdw_slab_range": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, _U64P, _U64P]),
     "fdw_owner_of": (C.c_int32, [C.c_uint64, _U64P, C.c_int32, C.c_int32]),
-    "fdw_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte * 128)]),
     "fdw_peer_export": (C.c_int, [_P, _P]),
     "fdw_peer_import": (C.c_int, [_P, _P, C.c_int32]),
     "fdw_peer_link": (C.c_int, [_P, _P, C.c_int32]),
@@ -96,29 +94,10 @@ EXPORTED = tuple(_SIGS)
 _lib = None
 
 
-def _preload_nccl():
-    """libfdwave_cuda.so links libnccl.so.2.  In a process that also uses
-    PyTorch, torch's bundled NCCL (newer) must be the one loaded: whichever
-    libnccl.so.2 comes first is shared by soname, and torch fails to import
-    against the older system copy.  So load the bundled one first, globally."""
-    try:
-        import importlib.util
-        spec = importlib.util.find_spec("nvidia.nccl")
-        for d in (spec.submodule_search_locations or []) if spec else []:
-            p = os.path.join(d, "lib", "libnccl.so.2")
-            if os.path.exists(p):
-                C.CDLL(p, mode=C.RTLD_GLOBAL)
-                return p
-    except Exception:
-        pass
-    return None
-
-
 def lib():
     """Loads libfdwave_cuda.so once; raises if it is absent (no CPU fallback)."""
     global _lib
     if _lib is None:
-        _preload_nccl()
         if not os.path.exists(LIB_PATH):
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"

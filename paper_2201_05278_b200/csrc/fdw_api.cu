@@ -4,14 +4,15 @@
 // device: layout and upload/download of the padded fields, source/receiver
 // index remapping, the step sequence (sweep -> inject -> swap -> boundary ->
 // health) captured as CUDA-graph chunks, and the Z-slab halo exchange over
-// NCCL for multi-GPU runs.  No CPU fallback: every compute path is a kernel.
+// NVLink peer memory for multi-GPU runs (no NCCL on the data path).  No CPU
+// fallback: every compute path is a kernel.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -146,7 +147,6 @@ struct fdw_solver {
     bool pdl_sweep = false;  // next TMA sweep launch: programmatic dependent launch (enqueue_step)
     unsigned long long capture_kernels = 0;
     unsigned long long launches = 0;  // kernels launched (graph nodes included)
-    ncclComm_t comm = nullptr;
     ProfileSink* prof = nullptr;
     // TMA descriptors (variant FDW_KERNEL_TMA): u-tile box for each level, and
     // the prev/c2dt2/eta tile box for each level, c2dt2 and eta
@@ -159,14 +159,9 @@ struct fdw_solver {
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev[2] = {nullptr, nullptr};
     cudaEvent_t rec_ev[2] = {nullptr, nullptr};
-    // slabs: the first and last Z segments are swept first (compute stream),
-    // their boundary planes exchanged on comm_s while the middle segments are
-    // swept on s2 (halo exchange overlapped with interior compute)
-    cudaStream_t s2 = nullptr, comm_s = nullptr;
-    cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
     std::vector<long long> h_tgt;             // host copy of the merged targets
     std::vector<std::vector<double>> h_tw;    // and their entry weights
-    int split_S = -1, n_tgt_a = 0;            // targets reordered: first/last-segment ones first
+    bool mirror_tgt = false;                  // a point-source target lies in a neighbour's ghost planes
     bool pending = false;
     unsigned long long pend_start = 0;
     int pend_cur = 0;
@@ -203,11 +198,15 @@ struct fdw_solver {
     size_t res_smem_base = 0;
     void* d_tapbuf = nullptr;
     int n_ent = 0;
-    // peer transport (Z slabs, world > 1 with an all-zero nccl_id): halo
-    // planes stored straight into the neighbours' levels over NVLink, step
-    // epochs and the health reduction through per-rank sync blocks
+    // peer transport (Z slabs, world > 1): halo planes stored straight into
+    // the neighbours' levels over NVLink, halo epochs and the health reduction
+    // through per-rank sync blocks
     bool peer_mode = false;
     bool peers_ready = false;
+    bool ipc_same_device = false;  // an IPC-imported neighbour shares this GPU (cannot step)
+    struct HostGroup* group = nullptr;  // host-ordered ranks (fdw_peer_link with a shared GPU)
+    bool no_pdl = false;           // FDW_NO_PDL at create time
+    bool tail_pdl_aware = false;   // last kernel of the previous step on `stream` is PDL-aware
     fdw::PeerSync* psync = nullptr;                        // own sync block (cudaMalloc, IPC-exportable)
     fdw::PeerSync* peer_sync[fdw::PEER_MAX_WORLD] = {};    // every rank's block, mapped
     void* peer_lvl[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [lower, upper][level], mapped
@@ -238,13 +237,6 @@ fdw_status fail(fdw_solver* c, fdw_status s, const char* fmt, ...) {
                         __FILE__, __LINE__);                                            \
     } while (0)
 
-#define NC(call)                                                                           \
-    do {                                                                                   \
-        ncclResult_t r_ = (call);                                                          \
-        if (r_ != ncclSuccess)                                                             \
-            return fail(c, FDW_ENCCL, "%s failed: %s", #call, ncclGetErrorString(r_));     \
-    } while (0)
-
 #define CHECK_LAUNCH()                      \
     do {                                    \
         CU(cudaGetLastError());             \
@@ -255,6 +247,67 @@ fdw_status fail(fdw_solver* c, fdw_status s, const char* fmt, ...) {
     } while (0)
 
 unsigned long long align_up(unsigned long long v, unsigned long long a) { return (v + a - 1) / a * a; }
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per function and process
+// wide: contexts on different host threads share it.  It is only ever raised
+// (a larger limit does not change occupancy), under one lock, so no thread can
+// lower it between another thread's set and launch.
+cudaError_t raise_smem_limit(const void* f, size_t bytes) {
+    static std::mutex mu;
+    static std::map<const void*, size_t> cur;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = cur[f];
+    if (bytes <= have) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
+
+}  // namespace
+
+// Ranks linked in one process whose GPUs are shared (one GPU emulating a
+// slab decomposition, e.g. the test suite) must never have a kernel spin on a
+// flag another launch on the same GPU sets: nothing guarantees the two run
+// concurrently.  Such a group is HOST-ORDERED: at every cross-rank point each
+// rank records an event, the rank threads meet at a host barrier, and each
+// stream waits on its peers' events before the kernel that checks the flags,
+// which then finds them already set.  Steps run as direct launches (no graph:
+// a captured graph cannot wait on another stream's per-step event).
+struct HostGroup {
+    int world = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    unsigned long long gen = 0;
+    bool broken = false;
+    fdw_solver* member[fdw::PEER_MAX_WORLD] = {};
+    cudaEvent_t ev[fdw::PEER_MAX_WORLD][2] = {};
+    unsigned long long round[fdw::PEER_MAX_WORLD] = {};
+    int alive = 0;
+    // false after 60 s without every rank arriving (a rank thread died or a
+    // caller skipped a collective call): the group is then broken for good
+    bool barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        if (broken) return false;
+        const unsigned long long g = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+            return true;
+        }
+        if (!cv.wait_for(lk, std::chrono::seconds(60), [&] { return gen != g || broken; })) broken = true;
+        if (broken) cv.notify_all();
+        return !broken;
+    }
+};
+
+namespace {
+std::mutex g_group_mu;
+std::map<const fdw_solver*, HostGroup*> g_groups;  // keyed by the rank-0 context
+}  // namespace
+
+namespace {
 
 // ---------------------------------------------------------------------------
 // kernel dispatch
@@ -370,9 +423,7 @@ SweepArgs<T> sweep_args(fdw_solver* c, int src, int dst) {
     }
     a.ctrl = c->ctrl;
     a.ezr = c->d_ezr;
-    a.seg_mul = 1;
-    a.seg_add = 0;
-    a.zseg_total = c->zseg;
+    a.seg_rot = 0;
     a.negz = static_cast<T>(-0.0);
     if (c->vd) {
         a.vd = 1;
@@ -489,20 +540,38 @@ const void* tma_kernel(int R, bool ex, int minb) {
     return nullptr;
 }
 
+fdw::PeerArgs peer_args(fdw_solver* c);
+bool fused_halo(const fdw_solver* c, bool virt);
+
 template <typename T, bool EX>
-bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst, int gz = 0, cudaStream_t st = nullptr) {
+bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
     using S4 = fdw::TmaShape<T, 4, TMA_BX>;
-    if (!st) st = c->stream;
+    const cudaStream_t st = c->stream;
     SweepArgs<T> a = a0;
-    if (c->peer_mode && c->peers_ready) {  // fused halo stores (see enqueue_step)
+    dim3 block(S4::NTY, TMA_BX);
+    dim3 grid((unsigned)((c->nyl + S4::TYW - 1) / S4::TYW), (unsigned)((c->nxl + TMA_BX - 1) / TMA_BX),
+              (unsigned)c->zseg);
+    if (fused_halo(c, true) && c->peers_ready) {
+        // the sweep runs the step's halo epoch (enqueue_step): boundary CTAs
+        // wait for the neighbours, store the halo planes into their ghost
+        // planes, and the last of them publishes; the boundary segments
+        // (S-1, 0) are rotated into the first wave
         a.peer_lo = static_cast<T*>(c->peer_lvl[0][dst]);
         a.peer_hi = static_cast<T*>(c->peer_lvl[1][dst]);
         a.peer_lo_delta = c->peer_delta[0];
         a.peer_hi_delta = c->peer_delta[1];
+        a.peer = peer_args(c);
+        a.publish = c->mirror_tgt ? 0 : 1;
+        const int S = c->zseg, R = c->R;
+        const long long nz = c->nzl;
+        unsigned nseg = 0;
+        for (int sg = 0; sg < S; ++sg) {
+            const long long zs = nz * sg / S, ze = nz * (sg + 1) / S;
+            if ((a.peer_lo && zs < R) || (a.peer_hi && ze > nz - R)) ++nseg;
+        }
+        a.n_bnd = nseg * grid.x * grid.y;
+        a.seg_rot = S - 1;
     }
-    dim3 block(S4::NTY, TMA_BX);
-    dim3 grid((unsigned)((c->nyl + S4::TYW - 1) / S4::TYW), (unsigned)((c->nxl + TMA_BX - 1) / TMA_BX),
-              (unsigned)(gz > 0 ? gz : c->zseg));
     const int col_base = (int)(c->base + c->R);
     const int smem = tma_smem<T>(c->R, c->vd);
     const CUtensorMap& g0 = c->tm_g[0];
@@ -519,7 +588,7 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst, int gz 
     cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = st;
     cfg.attrs = attr;
-    cfg.numAttrs = c->pdl_sweep && st == c->stream ? 1 : 0;
+    cfg.numAttrs = c->pdl_sweep ? 1 : 0;
     auto go = [&](auto kern) {
         // an error is left for the caller's CHECK_LAUNCH (cudaGetLastError)
         (void)cudaLaunchKernelEx(&cfg, kern, a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);
@@ -647,7 +716,7 @@ fdw_status launch_res2d_t(fdw_solver* c, int L, int cur0, bool record) {
         const void* f2 = res2d2_kernel<T>(c->R, ex);
         if (!f2) return fail(c, FDW_EINVAL, "resident 2D kernel not built for this configuration");
         // the smem attribute is per function, shared by every context of the process
-        CU(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem2));
+        CU(raise_smem_limit(f2, c->res_smem2));
         CU(cudaLaunchCooperativeKernel(f2, dim3((unsigned)c->res_nb), dim3(256), args2, c->res_smem2, c->stream));
         if (c->capturing)
             ++c->capture_kernels;
@@ -660,7 +729,7 @@ fdw_status launch_res2d_t(fdw_solver* c, int L, int cur0, bool record) {
         void* args[] = {&a, &Ls, &cur, &rec, &k0};
         const void* f = res2d_kernel<T>(c->R, ex);
         if (!f) return fail(c, FDW_EINVAL, "resident 2D kernel not built for this configuration");
-        CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem));
+        CU(raise_smem_limit(f, c->res_smem));
         CU(cudaLaunchCooperativeKernel(f, dim3((unsigned)c->res_nb), dim3(256), args, c->res_smem, c->stream));
         if (c->capturing)
             ++c->capture_kernels;
@@ -698,8 +767,8 @@ bool res2d_configure(fdw_solver* c) {
             const size_t smem1 =
                 (size_t)(2 * (BZ + 2 * R) * UW + 3 * BZ * TX) * sizeof(T) + 8 * fdw::F2D_CHUNK * sizeof(double);
             if (smem2 > 227 * 1024) continue;
-            if (cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) != cudaSuccess ||
-                cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1) != cudaSuccess) {
+            if (raise_smem_limit(f2, smem2) != cudaSuccess ||
+                raise_smem_limit(f, smem1) != cudaSuccess) {
                 cudaGetLastError();
                 continue;
             }
@@ -730,7 +799,7 @@ bool res2d_configure(fdw_solver* c) {
         const size_t smem =
             (size_t)(2 * (BZ + 2 * R) * UW + 3 * BZ * TX) * sizeof(T) + 8 * fdw::F2D_CHUNK * sizeof(double);
         if (smem > 227 * 1024) continue;
-        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        if (raise_smem_limit(f, smem) != cudaSuccess) {
             cudaGetLastError();
             continue;
         }
@@ -1068,8 +1137,6 @@ fdw_status launch_boundary(fdw_solver* c, int lv, int mode) {
     return c->tsize == 4 ? launch_boundary_t<float>(c, lv, mode) : launch_boundary_t<double>(c, lv, mode);
 }
 
-ncclDataType_t nccl_type(const fdw_solver* c) { return c->tsize == 4 ? ncclFloat : ncclDouble; }
-
 fdw::PeerArgs peer_args(fdw_solver* c) {
     fdw::PeerArgs p{};
     p.self = c->psync;
@@ -1080,56 +1147,131 @@ fdw::PeerArgs peer_args(fdw_solver* c) {
     return p;
 }
 
-// peer transport: signal this step's halo stores, wait for the neighbours'
-fdw_status launch_peer_sync(fdw_solver* c, cudaStream_t st) {
+bool slab_peers(const fdw_solver* c) { return c->d.world > 1 && c->peer_mode; }
+
+// Host-ordered group: this rank's stream waits for its neighbours' (or every
+// rank's) work enqueued before this point.  See HostGroup.
+fdw_status group_point(fdw_solver* c, bool all_ranks) {
+    HostGroup* g = c->group;
+    if (!g) return FDW_OK;
+    const int r = c->d.rank;
+    const int slot = (int)(g->round[r]++ & 1);
+    CU(cudaEventRecord(g->ev[r][slot], c->stream));
+    if (!g->barrier())
+        return fail(c, FDW_EPEER, "host-ordered slab group: a rank did not reach the same collective call within 60 s");
+    for (int s = 0; s < c->d.world; ++s) {
+        if (s == r || (!all_ranks && s != r - 1 && s != r + 1)) continue;
+        CU(cudaStreamWaitEvent(c->stream, g->ev[s][slot], 0));
+    }
+    return FDW_OK;
+}
+
+fdw_status peers_usable(fdw_solver* c) {
     if (!c->peers_ready) return fail(c, FDW_ESTATE, "peer transport: fdw_peer_import / fdw_peer_link first");
-    fdw::peer_halo_sync<<<1, 32, 0, st>>>(peer_args(c));
+    if (c->ipc_same_device)
+        return fail(c, FDW_ESTATE,
+                    "peer transport: a neighbour in another process shares this GPU; its kernels and ours would "
+                    "wait on each other -- drive ranks that share a GPU from one process (fdw_peer_link)");
+    return FDW_OK;
+}
+
+// Start of a halo epoch (before an operation that reads ghost planes or
+// stores into a neighbour's): wait until both neighbours published it.
+// `in_kernel`: the TMA sweep waits itself (only the host-ordered point here).
+fdw_status launch_peer_wait(fdw_solver* c, bool in_kernel, int honor_abort = 1) {
+    fdw_status s = peers_usable(c);
+    if (s) return s;
+    if ((s = group_point(c, false))) return s;
+    if (in_kernel) return FDW_OK;
+    fdw::peer_wait_kernel<<<1, 32, 0, c->stream>>>(peer_args(c), honor_abort);
     CHECK_LAUNCH();
     return FDW_OK;
 }
 
-// peer transport: copy the first / last R owned planes of level lv into the
-// neighbours' ghost planes (full padded planes), then synchronise.
-fdw_status launch_peer_push(fdw_solver* c, int lv, cudaStream_t st, bool sync = true) {
-    if (!c->peers_ready) return fail(c, FDW_ESTATE, "peer transport: fdw_peer_import / fdw_peer_link first");
+fdw_status launch_peer_publish(fdw_solver* c, int honor_abort = 1) {
+    fdw_status s = peers_usable(c);
+    if (s) return s;
+    fdw::peer_publish_kernel<<<1, 32, 0, c->stream>>>(peer_args(c), honor_abort);
+    CHECK_LAUNCH();
+    return FDW_OK;
+}
+
+// Copies the first / last R owned planes of level lv into the neighbours'
+// ghost planes (full padded planes); the caller brackets it with
+// launch_peer_wait / launch_peer_publish.
+fdw_status launch_peer_push(fdw_solver* c, int lv) {
+    fdw_status s = peers_usable(c);
+    if (s) return s;
     const long long n = (long long)c->R * c->plane;
     const long long lo_src = (long long)c->R * c->plane, hi_src = c->nzl * c->plane;
     const unsigned grid = (unsigned)std::min<long long>((n / (16 / c->tsize) + 255) / 256, (long long)c->sm_count * 4);
     if (c->tsize == 4)
-        fdw::peer_push<float><<<grid, 256, 0, st>>>(static_cast<const float*>(c->lvl[lv]),
-                                                     static_cast<float*>(c->peer_lvl[0][lv]),
-                                                     static_cast<float*>(c->peer_lvl[1][lv]), lo_src,
-                                                     c->peer_delta[0], hi_src, c->peer_delta[1], n);
+        fdw::peer_push<float><<<grid, 256, 0, c->stream>>>(static_cast<const float*>(c->lvl[lv]),
+                                                            static_cast<float*>(c->peer_lvl[0][lv]),
+                                                            static_cast<float*>(c->peer_lvl[1][lv]), lo_src,
+                                                            c->peer_delta[0], hi_src, c->peer_delta[1], n);
     else
-        fdw::peer_push<double><<<grid, 256, 0, st>>>(static_cast<const double*>(c->lvl[lv]),
-                                                      static_cast<double*>(c->peer_lvl[0][lv]),
-                                                      static_cast<double*>(c->peer_lvl[1][lv]), lo_src,
-                                                      c->peer_delta[0], hi_src, c->peer_delta[1], n);
+        fdw::peer_push<double><<<grid, 256, 0, c->stream>>>(static_cast<const double*>(c->lvl[lv]),
+                                                             static_cast<double*>(c->peer_lvl[0][lv]),
+                                                             static_cast<double*>(c->peer_lvl[1][lv]), lo_src,
+                                                             c->peer_delta[0], hi_src, c->peer_delta[1], n);
     CHECK_LAUNCH();
-    return sync ? launch_peer_sync(c, st) : FDW_OK;
+    return FDW_OK;
 }
 
-// Z-halo exchange: R planes per internal face, full padded planes (contiguous).
-fdw_status launch_halo(fdw_solver* c, int lv, cudaStream_t st = nullptr) {
-    if (c->d.world <= 1 || c->ndim != 3) return FDW_OK;
-    if (!st) st = c->stream;
-    if (c->peer_mode) return launch_peer_push(c, lv, st);
-    char* f = static_cast<char*>(c->lvl[lv]);
-    const size_t n = (size_t)c->R * c->plane;
-    const size_t bytes_plane = (size_t)c->plane * c->tsize;
-    const int rank = c->d.rank, world = c->d.world;
-    NC(ncclGroupStart());
-    if (rank > 0) {
-        NC(ncclSend(f + (size_t)c->R * bytes_plane, n, nccl_type(c), rank - 1, c->comm, st));
-        NC(ncclRecv(f, n, nccl_type(c), rank - 1, c->comm, st));
+// A whole halo epoch that only pushes level lv (refresh_boundary).
+fdw_status peer_exchange(fdw_solver* c, int lv) {
+    if (!slab_peers(c) || c->ndim != 3) return FDW_OK;
+    fdw_status s;
+    if ((s = launch_peer_wait(c, false, 0))) return s;
+    if ((s = launch_peer_push(c, lv))) return s;
+    return launch_peer_publish(c, 0);
+}
+
+// Teardown of a linked slab context, before its levels and sync block are
+// freed.  Host-ordered group: wait for the other members' queued work (their
+// stores into this rank's memory) and break the group, so a member that keeps
+// calling collectives fails at once instead of waiting for this rank.  Peer
+// ranks on other GPUs: a bounded device-side wait until every rank finished
+// the halo / health epochs this rank went through.
+void peer_leave(fdw_solver* c) {
+    if (!c->peer_mode || !c->peers_ready) return;
+    if (HostGroup* g = c->group) {
+        std::lock_guard<std::mutex> lk(g_group_mu);
+        {
+            std::lock_guard<std::mutex> gl(g->mu);
+            g->broken = true;
+            g->cv.notify_all();
+        }
+        for (int r = 0; r < g->world; ++r)
+            if (g->member[r] && g->member[r] != c) cudaStreamSynchronize(g->member[r]->stream);
+        g->member[c->d.rank] = nullptr;
+        c->group = nullptr;
+        if (--g->alive == 0) {
+            for (auto& e2 : g->ev)
+                for (cudaEvent_t e : e2)
+                    if (e) cudaEventDestroy(e);
+            for (auto it = g_groups.begin(); it != g_groups.end();)
+                it = it->second == g ? g_groups.erase(it) : std::next(it);
+            delete g;
+        }
+        return;
     }
-    if (rank < world - 1) {
-        NC(ncclSend(f + (size_t)(c->Lz - 2 * c->R) * bytes_plane, n, nccl_type(c), rank + 1, c->comm,
-                    st));
-        NC(ncclRecv(f + (size_t)(c->Lz - c->R) * bytes_plane, n, nccl_type(c), rank + 1, c->comm,
-                    st));
-    }
-    NC(ncclGroupEnd());
+    if (c->ipc_same_device) return;  // such a context never stepped (peers_usable)
+    fdw::peer_quiesce<<<1, 32, 0, c->stream>>>(peer_args(c), 5000000000ull);
+    cudaStreamSynchronize(c->stream);
+    cudaGetLastError();
+}
+
+// Cross-rank health reduction: post, (host-ordered point), reduce.
+fdw_status launch_peer_health(fdw_solver* c, int honor_abort) {
+    fdw_status s = peers_usable(c);
+    if (s) return s;
+    fdw::peer_health_post<<<1, 32, 0, c->stream>>>(peer_args(c), honor_abort);
+    CHECK_LAUNCH();
+    if ((s = group_point(c, true))) return s;
+    fdw::peer_health_reduce<<<1, 32, 0, c->stream>>>(peer_args(c), honor_abort);
+    CHECK_LAUNCH();
     return FDW_OK;
 }
 
@@ -1196,18 +1338,9 @@ fdw_status launch_health_t(fdw_solver* c, int lv, int honor_abort) {
             honor_abort);
         CHECK_LAUNCH();
     }
-    auto peer_reduce = [&]() -> fdw_status {
-        if (!c->peers_ready) return fail(c, FDW_ESTATE, "peer transport: fdw_peer_import / fdw_peer_link first");
-        fdw::peer_allreduce_health<<<1, 32, 0, c->stream>>>(peer_args(c));
-        CHECK_LAUNCH();
-        return FDW_OK;
-    };
-    if (c->d.world > 1 && c->peer_mode) {
-        fdw_status s = peer_reduce();
+    if (slab_peers(c)) {
+        fdw_status s = launch_peer_health(c, honor_abort);
         if (s) return s;
-    } else if (c->d.world > 1) {
-        NC(ncclAllReduce(&c->ctrl->bad_idx, &c->ctrl->bad_idx, 1, ncclUint64, ncclMin, c->comm, c->stream));
-        NC(ncclAllReduce(&c->ctrl->max_bits, &c->ctrl->max_bits, 1, ncclUint64, ncclMax, c->comm, c->stream));
     }
     {
         if (!raw) {
@@ -1221,20 +1354,16 @@ fdw_status launch_health_t(fdw_solver* c, int lv, int honor_abort) {
                                                              gp_lo, P1, P2, is3d, c->ctrl, honor_abort, raw ? 0 : 1);
         CHECK_LAUNCH();
     }
-    if (c->d.world > 1 && c->peer_mode) {
-        fdw_status s = peer_reduce();
+    if (slab_peers(c)) {
+        fdw_status s = launch_peer_health(c, honor_abort);
         if (s) return s;
-    } else if (c->d.world > 1) {
-        NC(ncclAllReduce(&c->ctrl->bad_idx, &c->ctrl->bad_idx, 1, ncclUint64, ncclMin, c->comm, c->stream));
     }
     fdw::health_classify<T><<<1, 1, 0, c->stream>>>(u, c->ctrl, c->origin_pad, c->ld, c->plane, gp_lo, gp_hi, P1, P2,
                                                     is3d, honor_abort);
     CHECK_LAUNCH();
-    if (c->d.world > 1 && c->peer_mode) {
-        fdw_status s = peer_reduce();
+    if (slab_peers(c)) {
+        fdw_status s = launch_peer_health(c, honor_abort);
         if (s) return s;
-    } else if (c->d.world > 1) {
-        NC(ncclAllReduce(&c->ctrl->kind, &c->ctrl->kind, 1, ncclUint32, ncclMax, c->comm, c->stream));
     }
     return FDW_OK;
 }
@@ -1373,7 +1502,7 @@ fdw_status res2d_receivers(fdw_solver* c, const std::vector<long long>& ri) {
         auto fits = [&](const void* f, size_t smem) {
             int got = 0;
             return smem <= 227 * 1024 &&
-                   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+                   raise_smem_limit(f, smem) == cudaSuccess &&
                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&got, f, 256, smem) == cudaSuccess &&
                    (long long)c->res_nb <= (long long)got * c->sm_count;
         };
@@ -1385,9 +1514,6 @@ fdw_status res2d_receivers(fdw_solver* c, const std::vector<long long>& ri) {
             c->res_tapcap = most;
             c->res_smem = s1;
             c->res_smem2 = s2;
-        } else {  // restore the attributes of the uncached sizes
-            cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem_base);
-            if (c->res_pair) cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem2_base);
         }
         cudaGetLastError();
     }
@@ -1400,115 +1526,54 @@ fdw_status res2d_receivers(fdw_solver* c, const std::vector<long long>& ri) {
     return FDW_OK;
 }
 
-// Sweep order for slabs: first/last Z segments, then exchange
-// their boundary planes while the middle segments are swept.
-bool split_step(const fdw_solver* c, bool virt) {
-    static const bool off = std::getenv("FDW_NO_HALO_OVERLAP") != nullptr;
-    static const bool force = std::getenv("FDW_FORCE_SPLIT") != nullptr;  // tests on one GPU
-    if (off || !virt || c->prof || c->variant != FDW_KERNEL_TMA || c->ndim != 3 || c->zseg < 3) return false;
-    if (c->peer_mode) return false;  // the sweep itself stores the halo planes
-    if (!c->vs_fields.empty() || !c->s2) return false;
-    if (c->nzl / c->zseg < c->R) return false;  // the exchanged planes must lie in the end segments
-    return c->d.world > 1 || force;
-}
-
-// Orders the targets so that those on planes of the first/last Z segment come
-// first (n_tgt_a of them); per-target entry order is untouched, so the
-// injection is unchanged -- only which launch applies it.
-fdw_status ensure_target_split(fdw_solver* c) {
-    const int S = c->zseg;
-    if (c->split_S == S) return FDW_OK;
-    std::vector<int> order_a, order_b;
-    for (size_t t = 0; t < c->h_tgt.size(); ++t) {
-        const long long z = (c->h_tgt[t] - c->origin) / c->plane;
-        const long long first_end = c->nzl * 1 / S, last_begin = c->nzl * (S - 1) / S;
-        ((z < first_end || z >= last_begin) ? order_a : order_b).push_back((int)t);
-    }
-    std::vector<long long> tg;
-    std::vector<unsigned int> eo(1, 0);
-    std::vector<double> ew;
-    for (const auto* ord : {&order_a, &order_b})
-        for (int t : *ord) {
-            tg.push_back(c->h_tgt[t]);
-            ew.insert(ew.end(), c->h_tw[t].begin(), c->h_tw[t].end());
-            eo.push_back((unsigned int)ew.size());
-        }
-    fdw_status s;
-    if ((s = dev_upload(c, &c->d_tgt, tg))) return s;
-    if ((s = dev_upload(c, &c->d_ent_off, eo))) return s;
-    if ((s = dev_upload(c, &c->d_ent_w, ew))) return s;
-    c->n_tgt_a = (int)order_a.size();
-    c->split_S = S;
-    return FDW_OK;
-}
-
-template <typename T>
-fdw_status enqueue_split_sweep_t(fdw_solver* c, int k, int src, int dst) {
-    const bool ex = c->d.math == FDW_MATH_EXACT;
-    const int S = c->zseg;
-    SweepArgs<T> a = sweep_args<T>(c, src, dst);
-    CU(cudaEventRecord(c->ev_start, c->stream));
-    CU(cudaStreamWaitEvent(c->s2, c->ev_start, 0));
-    // first and last segments (compute stream), then their point sources
-    a.seg_mul = S - 1;
-    a.seg_add = 0;
-    a.zseg_total = S;
-    if (!(ex ? launch_tma<T, true>(c, a, src, dst, 2) : launch_tma<T, false>(c, a, src, dst, 2)))
-        return fail(c, FDW_EINVAL, "TMA kernel not built for radius %d", c->R);
-    CHECK_LAUNCH();
-    fdw_status s;
-    if ((s = launch_inject_t<T>(c, dst, k, 0, c->n_tgt_a, c->stream))) return s;
-    CU(cudaEventRecord(c->ev_a, c->stream));
-    // boundary planes to the neighbours while the middle is swept
-    CU(cudaStreamWaitEvent(c->comm_s, c->ev_a, 0));
-    if ((s = launch_halo(c, dst, c->comm_s))) return s;
-    CU(cudaEventRecord(c->ev_c, c->comm_s));
-    a.seg_mul = 1;
-    a.seg_add = 1;
-    if (!(ex ? launch_tma<T, true>(c, a, src, dst, S - 2, c->s2) : launch_tma<T, false>(c, a, src, dst, S - 2, c->s2)))
-        return fail(c, FDW_EINVAL, "TMA kernel not built for radius %d", c->R);
-    CHECK_LAUNCH();
-    if ((s = launch_inject_t<T>(c, dst, k, c->n_tgt_a, -1, c->s2))) return s;
-    CU(cudaEventRecord(c->ev_b, c->s2));
-    CU(cudaStreamWaitEvent(c->stream, c->ev_b, 0));
-    CU(cudaStreamWaitEvent(c->stream, c->ev_c, 0));
-    return FDW_OK;
-}
-
 bool use_pdl(const fdw_solver* c) {
-    static const bool off = std::getenv("FDW_NO_PDL") != nullptr;
-    return !off && c->variant == FDW_KERNEL_TMA && c->d.world == 1 && !c->prof && c->vs_fields.empty();
+    // host-ordered groups put an event wait between steps: plain launches there
+    return !c->no_pdl && c->variant == FDW_KERNEL_TMA && !c->prof && c->vs_fields.empty() && !c->group;
 }
 
+// Whether the TMA sweep reading level `src` runs the slab's halo epoch itself
+// (waits in its boundary CTAs, stores the halo planes, publishes).
+bool fused_halo(const fdw_solver* c, bool virt) {
+    return slab_peers(c) && c->variant == FDW_KERNEL_TMA && virt && c->vs_fields.empty();
+}
+
+// One Solver::step (kernel.hpp:226-233) with relative index k inside a chunk;
+// `src` is the current level before the step.  For Z slabs the step is one
+// halo epoch: the neighbours' previous step must be complete before this
+// step's boundary CTAs read the ghost planes or store into theirs.
 fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
     const int dst = 1 - src;
     fdw_status s;
     const bool ovl = record && overlap_receivers(c);
     // this sweep overwrites level `dst`, which step k-2's receivers read
     if (ovl && k >= 2) CU(cudaStreamWaitEvent(c->stream, c->rec_ev[k & 1], 0));
-    if (split_step(c, virt)) {
-        // sweep + inject + halo exchange, overlapped (TMA: virtual ghosts, no faces)
-        s = c->tsize == 4 ? enqueue_split_sweep_t<float>(c, k, src, dst) : enqueue_split_sweep_t<double>(c, k, src, dst);
-        if (s) return s;
-    } else {
-        // programmatic dependent launch inside a chunk (single GPU, TMA sweep
-        // on virtual ghosts, no volume sources): the sweep follows the
-        // previous step's point-source kernel, which follows this sweep
-        const bool pdl = use_pdl(c) && virt;
-        c->pdl_sweep = pdl && k > 0;
-        { Mark m(c, 0); s = launch_sweep(c, src, dst, virt); c->pdl_sweep = false; if (s) return s; }
-        { Mark m(c, 1); if ((s = launch_inject(c, dst, k, pdl))) return s; }
-        // swap: dst is now the current level
-        if (!virt) { Mark m(c, 2); if ((s = launch_faces(c, dst))) return s; }
-        if (c->d.world > 1 && c->peer_mode) {
-            // the TMA sweep (virtual ghosts) and the point-source kernel stored
-            // the halo planes into the neighbours already; otherwise push them
-            Mark m(c, 5);
-            const bool fused = c->variant == FDW_KERNEL_TMA && virt && c->vs_fields.empty();
-            if ((s = fused ? launch_peer_sync(c, c->stream) : launch_peer_push(c, dst, c->stream))) return s;
-        } else if (c->d.world > 1) {
-            Mark m(c, 5);
-            if ((s = launch_halo(c, dst))) return s;
+    const bool peers = slab_peers(c) && c->ndim == 3;
+    const bool fused = fused_halo(c, virt);
+    if (peers && (s = launch_peer_wait(c, fused))) return s;
+    // programmatic dependent launch inside a chunk (TMA sweep on virtual
+    // ghosts, no volume sources): the sweep follows the previous step's
+    // point-source kernel (or sweep), which follows this sweep
+    const bool pdl = use_pdl(c) && virt;
+    c->pdl_sweep = pdl && k > 0 && c->tail_pdl_aware && !(peers && !fused);
+    { Mark m(c, 0); s = launch_sweep(c, src, dst, virt); c->pdl_sweep = false; if (s) return s; }
+    c->tail_pdl_aware = pdl;
+    if (c->n_tgt > 0 || !c->vs_fields.empty()) {
+        Mark m(c, 1);
+        if ((s = launch_inject(c, dst, k, pdl && c->tail_pdl_aware))) return s;
+        c->tail_pdl_aware = pdl && c->vs_fields.empty();
+    }
+    // swap: dst is now the current level
+    if (!virt) { Mark m(c, 2); if ((s = launch_faces(c, dst))) return s; c->tail_pdl_aware = false; }
+    if (peers) {
+        Mark m(c, 5);
+        if (!fused) {  // the sweep did not store the halo planes itself
+            if ((s = launch_peer_push(c, dst))) return s;
+        }
+        // the sweep publishes unless a point source wrote into the halo
+        // planes after it (its mirrored store must be visible first)
+        if (!fused || c->mirror_tgt) {
+            if ((s = launch_peer_publish(c))) return s;
+            c->tail_pdl_aware = false;
         }
     }
     if (record && ovl) {
@@ -1519,6 +1584,7 @@ fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
     } else if (record) {
         Mark m(c, 3);
         if ((s = launch_receivers(c, dst, k + 1))) return s;
+        c->tail_pdl_aware = false;
     }
     return FDW_OK;
 }
@@ -1526,6 +1592,7 @@ fdw_status enqueue_step(fdw_solver* c, int k, int src, bool record, bool virt) {
 fdw_status enqueue_chunk(fdw_solver* c, unsigned long long L, int cur0, bool check, bool record, bool first_virt,
                          bool rest_virt) {
     fdw_status s;
+    c->tail_pdl_aware = false;  // the chunk's first sweep follows an ordinary launch
     if (c->variant == FDW_KERNEL_FUSED2D) {
         // one cooperative launch for the chunk (one per step when profiling);
         // a raw first level takes one stored-ghost step first
@@ -1560,14 +1627,10 @@ fdw_status enqueue_chunk(fdw_solver* c, unsigned long long L, int cur0, bool che
 }
 
 fdw_status run_chunk(fdw_solver* c, unsigned long long L, bool check, bool record) {
-    if (split_step(c, true)) {  // (uploads; never inside a capture)
-        fdw_status s = ensure_target_split(c);
-        if (s) return s;
-    }
     const int cur0 = c->cur;
     const bool first_virt = virtual_step(c, c->gstate[cur0]);
     const bool rest_virt = virtual_step(c, 0);
-    if (L < 8 || c->prof || c->variant == FDW_KERNEL_FUSED2D) {
+    if (L < 8 || c->prof || c->variant == FDW_KERNEL_FUSED2D || c->group) {
         fdw_status s = enqueue_chunk(c, L, cur0, check, record, first_virt, rest_virt);
         if (s) return s;
     } else {
@@ -1786,7 +1849,9 @@ fdw_status resolve_pending(fdw_solver* c, uint64_t* bad_step, double* bad_max) {
     if ((s = read_ctrl(c))) return s;
     if (!c->h_ctrl->abort) return FDW_OK;
     if (c->h_ctrl->peer_err)
-        return fail(c, FDW_ECUDA, "peer transport: a neighbour did not signal within 20 s (rank %d of %d)",
+        return fail(c, FDW_EPEER,
+                    "peer transport: a rank of the slab decomposition failed or did not signal within 20 s "
+                    "(seen by rank %d of %d)",
                     c->d.rank, c->d.world);
     const unsigned long long done = c->h_ctrl->step - c->pend_start;
     c->host_step = c->h_ctrl->step;
@@ -1844,7 +1909,7 @@ const char* fdw_status_string(fdw_status s) {
         case FDW_OK: return "ok";
         case FDW_EINVAL: return "invalid argument";
         case FDW_ECUDA: return "CUDA error";
-        case FDW_ENCCL: return "NCCL error";
+        case FDW_EPEER: return "peer transport error";
         case FDW_EINSTABLE: return "non-finite wavefield";
         case FDW_ENOMEM: return "out of memory";
         case FDW_ESTATE: return "invalid call order";
@@ -1880,6 +1945,7 @@ struct PeerBlob {
     int64_t ld, plane, nzl, origin, pid;
     cudaIpcMemHandle_t lvl[2];
     cudaIpcMemHandle_t sync;
+    char bus[32];  // PCI bus id of the rank's GPU (ordinals differ between processes)
 };
 static_assert(sizeof(PeerBlob) <= FDW_PEER_BLOB_BYTES, "peer blob size");
 constexpr uint32_t PEER_MAGIC = 0x50574446u;  // "FDWP"
@@ -1916,6 +1982,7 @@ fdw_status fdw_peer_export(fdw_solver* c, unsigned char out[FDW_PEER_BLOB_BYTES]
     b.nzl = c->nzl;
     b.origin = c->origin;
     b.pid = (int64_t)getpid();
+    CU(cudaDeviceGetPCIBusId(b.bus, (int)sizeof(b.bus), c->d.device));
     for (int l = 0; l < 2; ++l) CU(cudaIpcGetMemHandle(&b.lvl[l], c->lvl[l]));
     CU(cudaIpcGetMemHandle(&b.sync, c->psync));
     std::memset(out, 0, FDW_PEER_BLOB_BYTES);
@@ -1929,6 +1996,8 @@ fdw_status fdw_peer_import(fdw_solver* c, const unsigned char* blobs, int32_t wo
     if (!c->peer_mode) return fail(c, FDW_EINVAL, "not a peer-transport slab context");
     if (!blobs || world != c->d.world) return fail(c, FDW_EINVAL, "need one blob per rank (%d)", c->d.world);
     if (c->peers_ready) return fail(c, FDW_ESTATE, "peers already imported");
+    char bus[32] = {};
+    CU(cudaDeviceGetPCIBusId(bus, (int)sizeof(bus), c->d.device));
     for (int r = 0; r < world; ++r) {
         if (r == c->d.rank) continue;
         PeerBlob b;
@@ -1938,6 +2007,7 @@ fdw_status fdw_peer_import(fdw_solver* c, const unsigned char* blobs, int32_t wo
         if (b.pid == (int64_t)getpid())
             return fail(c, FDW_EINVAL, "peer rank %d lives in this process: use fdw_peer_link", r);
         if ((s = peer_geometry(c, r, b.ld, b.plane, b.nzl, b.origin, b.tsize, b.R))) return s;
+        if (std::strncmp(b.bus, bus, sizeof(bus)) == 0) c->ipc_same_device = true;
         void* p = nullptr;
         CU(cudaIpcOpenMemHandle(&p, b.sync, cudaIpcMemLazyEnablePeerAccess));
         c->ipc_mapped.push_back(p);
@@ -1980,15 +2050,25 @@ fdw_status fdw_peer_link(fdw_solver* c, fdw_solver* const* all, int32_t world) {
         if (side >= 0)
             for (int l = 0; l < 2; ++l) c->peer_lvl[side][l] = o->lvl[l];
     }
+    // ranks sharing a GPU (or FDW_PEER_HOST_ORDER=1): host-ordered group
+    bool shared = std::getenv("FDW_PEER_HOST_ORDER") != nullptr;
+    for (int r = 0; r < world; ++r)
+        for (int q = r + 1; q < world; ++q) shared = shared || all[r]->d.device == all[q]->d.device;
+    if (shared) {
+        std::lock_guard<std::mutex> lk(g_group_mu);
+        HostGroup*& g = g_groups[all[0]];
+        if (!g) {
+            g = new HostGroup();
+            g->world = world;
+        }
+        const int r = c->d.rank;
+        for (int k = 0; k < 2; ++k)
+            if (!g->ev[r][k]) CU(cudaEventCreateWithFlags(&g->ev[r][k], cudaEventDisableTiming));
+        g->member[r] = c;
+        ++g->alive;
+        c->group = g;
+    }
     c->peers_ready = true;
-    return FDW_OK;
-}
-
-fdw_status fdw_nccl_unique_id(unsigned char out[128]) {
-    ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess) return FDW_ENCCL;
-    static_assert(sizeof(id) == 128, "ncclUniqueId size");
-    std::memcpy(out, &id, 128);
     return FDW_OK;
 }
 
@@ -2098,12 +2178,6 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
     if (!ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream")) return bail(FDW_ECUDA);
     c->own_stream = true;
     if (!ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream")) return bail(FDW_ECUDA);
-    if (d.ndim == 3) {
-        if (!ck(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking), "stream")) return bail(FDW_ECUDA);
-        if (!ck(cudaStreamCreateWithFlags(&c->comm_s, cudaStreamNonBlocking), "stream")) return bail(FDW_ECUDA);
-        for (cudaEvent_t* e : {&c->ev_start, &c->ev_a, &c->ev_b, &c->ev_c})
-            if (!ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event")) return bail(FDW_ECUDA);
-    }
     for (int k = 0; k < 2; ++k) {
         if (!ck(cudaEventCreateWithFlags(&c->fork_ev[k], cudaEventDisableTiming), "event")) return bail(FDW_ECUDA);
         if (!ck(cudaEventCreateWithFlags(&c->rec_ev[k], cudaEventDisableTiming), "event")) return bail(FDW_ECUDA);
@@ -2121,11 +2195,8 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
     }
-    if (c->ndim == 3 && d.world > 1) {
-        bool zero_id = true;
-        for (unsigned char b : d.nccl_id) zero_id = zero_id && b == 0;
-        c->peer_mode = zero_id;
-    }
+    c->peer_mode = c->ndim == 3 && d.world > 1;
+    c->no_pdl = std::getenv("FDW_NO_PDL") != nullptr;
     for (void** p : {&c->lvl[0], &c->lvl[1], &c->c2dt2, &c->eta}) {
         // peer transport: the levels are mapped by the neighbours (cudaIpc
         // needs cudaMalloc memory, not the stream-ordered pool)
@@ -2208,7 +2279,7 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
             c->tma_minb = minb;
             const void* f = c->tsize == 4 ? tma_kernel<float>(R, ex, minb) : tma_kernel<double>(R, ex, minb);
             const int smem = c->tsize == 4 ? tma_smem<float>(R) : tma_smem<double>(R);
-            if (!ck(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr"))
+            if (!ck(raise_smem_limit(f, smem), "smem attr"))
                 return bail(FDW_ECUDA);
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 16 * TMA_BX, smem) != cudaSuccess || occ < 1)
                 occ = 1;
@@ -2218,15 +2289,6 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
         if (c->zseg > c->nzl) c->zseg = (int)c->nzl;
     }
 
-    if (c->d.world > 1 && !c->peer_mode) {
-        ncclUniqueId id;
-        std::memcpy(&id, d.nccl_id, sizeof(id));
-        ncclResult_t r = ncclCommInitRank(&c->comm, c->d.world, id, c->d.rank);
-        if (r != ncclSuccess) {
-            fail(c, FDW_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
-            return bail(FDW_ENCCL);
-        }
-    }
     pt.lap("kernel_setup");
     if (!ck(cudaStreamSynchronize(c->stream), "sync")) return bail(FDW_ECUDA);
     pt.lap("sync");
@@ -2255,13 +2317,9 @@ fdw_status fdw_destroy(fdw_solver* c) {
         if (c->rec_ev[k]) cudaEventDestroy(c->rec_ev[k]);
     }
     if (c->side) cudaStreamDestroy(c->side);
-    for (cudaEvent_t e : {c->ev_start, c->ev_a, c->ev_b, c->ev_c})
-        if (e) cudaEventDestroy(e);
-    for (cudaStream_t st : {c->s2, c->comm_s})
-        if (st) cudaStreamDestroy(st);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     lap("graphs");
-    if (c->comm) ncclCommDestroy(c->comm);
+    peer_leave(c);
     for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
     if (c->peer_mode) {
         if (c->stream) cudaStreamSynchronize(c->stream);
@@ -2372,7 +2430,7 @@ fdw_status fdw_set_density(fdw_solver* c, const void* rho, int on_device) {
         const bool ex = c->d.math == FDW_MATH_EXACT;
         const void* f = c->tsize == 4 ? tma_vd_kernel<float>(c->R, ex) : tma_vd_kernel<double>(c->R, ex);
         const int smem = c->tsize == 4 ? tma_smem<float>(c->R, true) : tma_smem<double>(c->R, true);
-        CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CU(raise_smem_limit(f, smem));
         int occ = 1;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 16 * TMA_BX, smem) != cudaSuccess || occ < 1)
             occ = 1;
@@ -2489,8 +2547,15 @@ fdw_status fdw_set_sources(fdw_solver* c, uint64_t n_points, const uint64_t* off
     }
     c->h_tgt = tgt;
     c->h_tw = ws;
-    c->split_S = -1;
-    c->n_tgt_a = 0;
+    // a target in the first / last R owned planes is also a neighbour's ghost
+    // cell: the point-source kernel mirrors it, and the step publishes after it
+    c->mirror_tgt = false;
+    if (c->ndim == 3 && c->d.world > 1)
+        for (long long o : tgt) {
+            const long long z = (o - c->origin) / c->plane;
+            if ((c->d.rank > 0 && z < c->R) || (c->d.rank < c->d.world - 1 && z >= c->nzl - c->R))
+                c->mirror_tgt = true;
+        }
     if ((s = dev_upload(c, &c->d_tgt, tgt))) return s;
     if ((s = dev_upload(c, &c->d_ent_off, eo))) return s;
     if ((s = dev_upload(c, &c->d_ent_w, ew))) return s;
@@ -2602,7 +2667,7 @@ fdw_status fdw_refresh_boundary(fdw_solver* c) {
     fdw_status s = enter(c);
     if (s) return s;
     if ((s = launch_boundary(c, c->cur, 0))) return s;
-    if ((s = launch_halo(c, c->cur))) return s;
+    if ((s = peer_exchange(c, c->cur))) return s;
     c->gstate[c->cur] = 0;
     CU(cudaStreamSynchronize(c->stream));
     return FDW_OK;

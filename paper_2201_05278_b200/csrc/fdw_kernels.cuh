@@ -32,6 +32,131 @@ struct Ctrl {
 };
 
 // ---------------------------------------------------------------------------
+// Peer transport for Z slabs (one GPU per rank on one NVLink/NVSwitch box).
+// A rank's first / last R owned planes are the lower / upper neighbour's ghost
+// planes; they are stored straight into the neighbour's level through mapped
+// peer memory (by the sweep epilogue, by the point-source kernel for targets
+// in those planes, or by peer_push).  No NCCL on the data path.
+//
+// Ordering is one halo epoch per collective operation (a step, a refresh, an
+// upload): before an operation reads its ghost planes or stores into a
+// neighbour's, it waits until both neighbours have PUBLISHED the epoch this
+// rank is at (they finished the previous operation: their stores into this
+// rank's ghost planes are visible, and they are done reading the buffer this
+// rank writes into next); when its own boundary work is done it publishes
+// epoch + 1.  In a TMA step both halves live inside the sweep: the CTAs that
+// touch the first / last R planes wait at their start and the last of them to
+// finish publishes, so no separate launch and no kernel-wide spin is needed.
+template <typename T>
+struct PeerMirror {
+    T* lo = nullptr;             // lower neighbour's level (mapped), or null
+    T* hi = nullptr;             // upper neighbour's level (mapped), or null
+    long long lo_delta = 0, hi_delta = 0;  // neighbour element = local element + delta
+    long long lo_end = 0;        // local elements [origin, lo_end) lie in the first R planes
+    long long hi_begin = 0;      // local elements >= hi_begin lie in the last R planes
+    __device__ __forceinline__ void store(long long i, T v) const {
+        if (lo && i < lo_end) lo[i + lo_delta] = v;
+        if (hi && i >= hi_begin) hi[i + hi_delta] = v;
+    }
+};
+
+constexpr int PEER_MAX_WORLD = 8;
+// Per-rank synchronisation block (device memory, IPC-exported).  Flags are
+// written by the other ranks with st.release.sys and read with ld.acquire.sys.
+struct PeerSync {
+    unsigned long long halo_flag[PEER_MAX_WORLD];    // halo epoch last published by rank s
+    unsigned long long health_flag[PEER_MAX_WORLD];  // health epoch last posted by rank s
+    unsigned long long in_idx[2][PEER_MAX_WORLD];    // health inbox (epoch parity, source rank)
+    unsigned long long in_max[2][PEER_MAX_WORLD];
+    unsigned int in_kind[2][PEER_MAX_WORLD];
+    unsigned long long halo_epoch;                   // this rank's own counters
+    unsigned long long health_epoch;
+    unsigned int bnd_done;                           // boundary CTAs of the running sweep that finished
+    unsigned int abort_word;                         // sticky: some rank hit a peer failure (any rank may set it)
+};
+
+struct PeerArgs {
+    PeerSync* self;
+    PeerSync* peer[PEER_MAX_WORLD];  // mapped sync blocks of every rank (peer[rank] = self)
+    int rank, world;
+    Ctrl* ctrl;
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned int ld_volatile_u32(const unsigned int* p) {
+    return *reinterpret_cast<const volatile unsigned int*>(p);
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// A peer failure is made visible to EVERY rank: the sticky abort word is set in
+// each rank's sync block, and every later wait on any rank sees it and latches
+// its own abort (so no rank keeps stepping on frozen ghost planes).
+__device__ void peer_fail(PeerSync* const* peer, int world, Ctrl* ctrl) {
+    ctrl->peer_err = 1u;
+    ctrl->abort = 1u;
+    for (int s = 0; s < world; ++s)
+        if (peer[s]) atomicExch_system(&peer[s]->abort_word, 1u);
+    __threadfence_system();
+}
+__device__ __forceinline__ bool peer_aborted(const PeerSync* self, Ctrl* ctrl) {
+    if (ld_volatile_u32(&self->abort_word) == 0u) return false;
+    ctrl->peer_err = 1u;
+    ctrl->abort = 1u;
+    return true;
+}
+
+// Spins (one thread) until *flag >= want.  A failure anywhere (sticky word) or
+// ~20 s without progress turns into peer_err + abort on every rank instead of
+// a hung device.
+__device__ bool peer_wait_flag(const unsigned long long* flag, unsigned long long want, PeerSync* const* peer,
+                               int world, const PeerSync* self, Ctrl* ctrl) {
+    if (peer_aborted(self, ctrl)) return false;
+    if (ld_acquire_sys(flag) >= want) return true;
+    const unsigned long long t0 = global_ns();
+    unsigned int ns = 32;
+    while (ld_acquire_sys(flag) < want) {
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
+        if (peer_aborted(self, ctrl)) return false;
+        if (global_ns() - t0 > 20000000000ull) {
+            peer_fail(peer, world, ctrl);
+            return false;
+        }
+    }
+    return true;
+}
+
+// Waits until both neighbours have published this rank's current halo epoch.
+__device__ __forceinline__ bool peer_wait_neighbours(const PeerArgs& p) {
+    const unsigned long long want = p.self->halo_epoch;
+    if (p.rank > 0 && !peer_wait_flag(&p.self->halo_flag[p.rank - 1], want, p.peer, p.world, p.self, p.ctrl))
+        return false;
+    if (p.rank < p.world - 1 &&
+        !peer_wait_flag(&p.self->halo_flag[p.rank + 1], want, p.peer, p.world, p.self, p.ctrl))
+        return false;
+    return true;
+}
+// Publishes epoch + 1 to both neighbours (after this rank's boundary work).
+__device__ __forceinline__ void peer_publish(const PeerArgs& p) {
+    const unsigned long long e = p.self->halo_epoch + 1;
+    p.self->halo_epoch = e;
+    __threadfence_system();
+    if (p.rank > 0) st_release_sys(&p.peer[p.rank - 1]->halo_flag[p.rank], e);
+    if (p.rank < p.world - 1) st_release_sys(&p.peer[p.rank + 1]->halo_flag[p.rank], e);
+}
+
+// ---------------------------------------------------------------------------
 template <typename T, bool EXACT>
 struct Ar;
 template <>
@@ -130,19 +255,22 @@ struct SweepArgs {
     // TMA sweep: per tile column, the Z range [x, y) of planes whose eta tile
     // is all zero (those planes skip the eta stream); null: none
     const int2* ezr;
-    T negz;
-    // TMA sweep Z segments: CTA z-index b sweeps segment b*seg_mul + seg_add
-    // of zseg_total over [0, nz) (1, 0, gridDim.z: all; S-1, 0, S with
-    // gridDim.z = 2: the first and last; 1, 1, S with gridDim.z = S-2: the
-    // middle).  Used to sweep a slab's boundary planes first and exchange them
-    // while the interior is swept.
-    int seg_mul, seg_add, zseg_total;  // -0 (runtime value for the packed exact products)
+    // TMA sweep Z segments: CTA z-index b sweeps segment (b + seg_rot) mod
+    // gridDim.z; a slab rotates its boundary segments (S-1, 0) into the first
+    // wave so the halo stores and the epoch publish happen early in the step.
+    int seg_rot;
     // peer transport (Z slabs over NVLink peer memory): the TMA sweep also
     // stores its first / last R planes into the lower / upper neighbour's ghost
-    // planes of the same level, at element (local index + delta); null: none
+    // planes of the same level, at element (local index + delta); null: none.
+    // The CTAs that touch those planes wait for the neighbours' epoch first;
+    // the last of the n_bnd of them publishes the next epoch (publish = 1).
     T* peer_lo;
     T* peer_hi;
     long long peer_lo_delta, peer_hi_delta;
+    PeerArgs peer;
+    unsigned int n_bnd;
+    int publish;
+    T negz;  // -0 (runtime value for the packed exact products)
     const Ctrl* ctrl;
 };
 
@@ -476,7 +604,8 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
     const int y0 = ty0 + ty * V;
     const int x = tx0 + tx;
     const int nz = a.nz, nx = a.nx, ny = a.ny;
-    const int seg = (int)blockIdx.z * a.seg_mul + a.seg_add, nseg = a.zseg_total;
+    const int nseg = (int)gridDim.z;
+    const int seg = ((int)blockIdx.z + a.seg_rot) % nseg;
     const int zs = (int)((long long)nz * seg / nseg);
     const int ze = (int)((long long)nz * (seg + 1) / nseg);
     const long long plane = a.plane;
@@ -533,6 +662,16 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
     // everything above touches shared memory and setup-time data only
     pdl_wait();
     if (a.ctrl->abort) return;
+    // peer transport: this CTA reads ghost planes written by a neighbour and
+    // stores into the neighbour's -> the neighbours must have published this
+    // rank's epoch (they finished the previous step)
+    const bool plo = a.peer_lo && zs < R, phi = a.peer_hi && ze > nz - R;
+    if (plo || phi) {
+        __shared__ int peer_ok;
+        if (tid == 0) peer_ok = peer_wait_neighbours(a.peer) ? 1 : 0;
+        __syncthreads();
+        if (!peer_ok) return;
+    }
     if (tid == 0) {
         for (int k = 0; k <= R; ++k) issue_u(k);  // planes zs .. zs+R
         issue_p(0);
@@ -798,7 +937,6 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
     // re-reads its own just-written outputs; outside the plane loop, so the
     // hot loop's registers are untouched), performed system-wide before the
     // grid ends
-    const bool plo = a.peer_lo && zs < R, phi = a.peer_hi && ze > nz - R;
     if ((plo || phi) && xin) {
         auto copy_plane = [&](T* peer, long long delta, int z) {
             const T* o = a.out + col0 + (long long)z * plane;
@@ -815,7 +953,15 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
         if (phi)
             for (int z = max(zs, nz - R); z < ze; ++z) copy_plane(a.peer_hi, a.peer_hi_delta, z);
     }
-    if (plo || phi) __threadfence_system();
+    if (plo || phi) {
+        // the last boundary CTA of the step publishes the next epoch
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0 && a.publish && atomicAdd(&a.peer.self->bnd_done, 1u) == a.n_bnd - 1) {
+            a.peer.self->bnd_done = 0u;
+            peer_publish(a.peer);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1894,99 +2040,49 @@ __global__ void density_grad_kernel(const T* __restrict__ rho, T* __restrict__ g
     g[i] = static_cast<T>(__ddiv_rn(__dmul_rn(acc, inv2h), static_cast<double>(rho[i])));
 }
 
-// ---------------------------------------------------------------------------
-// Peer transport for Z slabs (one process per GPU on one NVLink/NVSwitch box).
-// A rank's first / last R owned planes are the lower / upper neighbour's ghost
-// planes; they are stored straight into the neighbour's level through mapped
-// peer memory (by the sweep epilogue, by the point-source kernel for targets
-// in those planes, or by peer_push), then one thread per rank signals and
-// waits on step-epoch flags (peer_halo_sync).  No NCCL on the data path.
-template <typename T>
-struct PeerMirror {
-    T* lo = nullptr;             // lower neighbour's level (mapped), or null
-    T* hi = nullptr;             // upper neighbour's level (mapped), or null
-    long long lo_delta = 0, hi_delta = 0;  // neighbour element = local element + delta
-    long long lo_end = 0;        // local elements [origin, lo_end) lie in the first R planes
-    long long hi_begin = 0;      // local elements >= hi_begin lie in the last R planes
-    __device__ __forceinline__ void store(long long i, T v) const {
-        if (lo && i < lo_end) lo[i + lo_delta] = v;
-        if (hi && i >= hi_begin) hi[i + hi_delta] = v;
-    }
-};
-
-constexpr int PEER_MAX_WORLD = 8;
-// Per-rank synchronisation block (device memory, IPC-exported).  Flags are
-// written by the other ranks with st.release.sys and read with ld.acquire.sys.
-struct PeerSync {
-    unsigned long long halo_flag[PEER_MAX_WORLD];    // halo epoch last signalled by rank s
-    unsigned long long health_flag[PEER_MAX_WORLD];  // health epoch last signalled by rank s
-    unsigned long long in_idx[2][PEER_MAX_WORLD];    // health inbox (epoch parity, source rank)
-    unsigned long long in_max[2][PEER_MAX_WORLD];
-    unsigned int in_kind[2][PEER_MAX_WORLD];
-    unsigned long long halo_epoch;                   // this rank's own counters
-    unsigned long long health_epoch;
-};
-
-struct PeerArgs {
-    PeerSync* self;
-    PeerSync* peer[PEER_MAX_WORLD];  // mapped sync blocks of every rank (peer[rank] = self)
-    int rank, world;
-    Ctrl* ctrl;
-};
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// Halo epoch halves as separate launches, for operations whose kernels do not
+// wait / publish themselves (stored-ghost and non-TMA sweeps, uploads,
+// refresh_boundary, point sources mirrored into a neighbour).
+__global__ void peer_wait_kernel(PeerArgs p, int honor_abort) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (honor_abort && p.ctrl->abort) return;
+    peer_wait_neighbours(p);
 }
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
+__global__ void peer_publish_kernel(PeerArgs p, int honor_abort) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (honor_abort && p.ctrl->abort) return;
+    peer_publish(p);
 }
-__device__ __forceinline__ unsigned long long global_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-// Spins (one thread) until *flag >= want; after ~20 s latches peer_err + abort
-// instead of hanging the device.
-__device__ bool peer_wait_flag(const unsigned long long* flag, unsigned long long want, Ctrl* ctrl) {
+
+// Teardown handshake: before a rank frees the memory its neighbours map, it
+// waits (bounded; no abort latched) until every rank has finished the halo and
+// health epochs this rank went through, so no neighbour store is in flight.
+__global__ void peer_quiesce(PeerArgs p, unsigned long long timeout_ns) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const unsigned long long t0 = global_ns();
-    unsigned int ns = 32;
-    while (ld_acquire_sys(flag) < want) {
-        __nanosleep(ns);
-        if (ns < 1024) ns <<= 1;
-        if (global_ns() - t0 > 20000000000ull) {
-            ctrl->peer_err = 1u;
-            ctrl->abort = 1u;
-            return false;
+    auto reach = [&](const unsigned long long* f, unsigned long long want) {
+        while (ld_acquire_sys(f) < want) {
+            if (ld_volatile_u32(&p.self->abort_word) || global_ns() - t0 > timeout_ns) return false;
+            __nanosleep(1024);
         }
+        return true;
+    };
+    for (int s = 0; s < p.world; ++s) {
+        if (s == p.rank) continue;
+        if ((s == p.rank - 1 || s == p.rank + 1) && !reach(&p.self->halo_flag[s], p.self->halo_epoch)) return;
+        if (!reach(&p.self->health_flag[s], p.self->health_epoch)) return;
     }
-    return true;
 }
 
-// After a step's writes into the neighbours' ghost planes: signal them, then
-// wait until both neighbours have signalled the same epoch (their writes into
-// this rank's ghost planes are visible, and they are done reading the level
-// this rank writes next).  Runs whether or not the step was aborted, so the
-// epochs of all ranks stay in step.
-__global__ void peer_halo_sync(PeerArgs p) {
+// Health reduction across ranks (kernel.hpp:456-458 over all slabs): every
+// rank posts its (first non-finite index, max |u| bits, kind) into each other
+// rank's inbox slot (double-buffered by epoch parity) and signals; the reduce
+// half waits for all ranks and combines locally.  Two launches so that a
+// host-ordered group can put its cross-rank event between them.
+__global__ void peer_health_post(PeerArgs p, int honor_abort) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const unsigned long long e = p.self->halo_epoch + 1;
-    p.self->halo_epoch = e;
-    __threadfence_system();
-    if (p.rank > 0) st_release_sys(&p.peer[p.rank - 1]->halo_flag[p.rank], e);
-    if (p.rank < p.world - 1) st_release_sys(&p.peer[p.rank + 1]->halo_flag[p.rank], e);
-    if (p.rank > 0 && !peer_wait_flag(&p.self->halo_flag[p.rank - 1], e, p.ctrl)) return;
-    if (p.rank < p.world - 1) peer_wait_flag(&p.self->halo_flag[p.rank + 1], e, p.ctrl);
-}
-
-// Health reduction across ranks (replaces the ncclAllReduce min/max calls):
-// every rank stores its (first non-finite index, max |u| bits, kind) into each
-// other rank's inbox slot, signals, waits for all, then reduces locally.
-__global__ void peer_allreduce_health(PeerArgs p) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (honor_abort && p.ctrl->abort) return;
     const unsigned long long e = p.self->health_epoch + 1;
-    p.self->health_epoch = e;
     const int slot = (int)(e & 1);
     const unsigned long long idx = p.ctrl->bad_idx, mx = p.ctrl->max_bits;
     const unsigned int kind = p.ctrl->kind;
@@ -2000,11 +2096,18 @@ __global__ void peer_allreduce_health(PeerArgs p) {
     __threadfence_system();
     for (int s = 0; s < p.world; ++s)
         if (s != p.rank) st_release_sys(&p.peer[s]->health_flag[p.rank], e);
-    unsigned long long r_idx = idx, r_max = mx;
-    unsigned int r_kind = kind;
+}
+__global__ void peer_health_reduce(PeerArgs p, int honor_abort) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (honor_abort && p.ctrl->abort) return;
+    const unsigned long long e = p.self->health_epoch + 1;
+    p.self->health_epoch = e;
+    const int slot = (int)(e & 1);
+    unsigned long long r_idx = p.ctrl->bad_idx, r_max = p.ctrl->max_bits;
+    unsigned int r_kind = p.ctrl->kind;
     for (int s = 0; s < p.world; ++s) {
         if (s == p.rank) continue;
-        if (!peer_wait_flag(&p.self->health_flag[s], e, p.ctrl)) return;
+        if (!peer_wait_flag(&p.self->health_flag[s], e, p.peer, p.world, p.self, p.ctrl)) return;
         r_idx = min(r_idx, p.self->in_idx[slot][s]);
         r_max = max(r_max, p.self->in_max[slot][s]);
         r_kind = max(r_kind, p.self->in_kind[slot][s]);
@@ -2012,6 +2115,7 @@ __global__ void peer_allreduce_health(PeerArgs p) {
     p.ctrl->bad_idx = r_idx;
     p.ctrl->max_bits = r_max;
     p.ctrl->kind = r_kind;
+    peer_aborted(p.self, p.ctrl);  // a failure on any rank surfaces at every check
 }
 
 // Copies this rank's first / last R owned planes (full padded planes,

@@ -1,11 +1,10 @@
 """Multi-GPU host plumbing for the Z-slab decomposition (one process per GPU).
 
-The library owns the data path: with the peer transport (default) the sweep
-stores the R halo planes straight into the neighbours' levels over NVLink peer
-memory; with the NCCL transport they are exchanged by send/recv inside the step
-graph (fdw_api.cu launch_halo).  This module only does the control-plane work
-around it with torch.distributed:
-  * all-gather the peer IPC blobs (link_peers) or broadcast the NCCL unique id,
+The library owns the data path: the sweep stores the R halo planes straight
+into the neighbours' levels over NVLink peer memory and orders the steps with
+halo epochs in per-rank sync blocks (fdw_api.cu enqueue_step).  This module only
+does the control-plane work around it with torch.distributed:
+  * all-gather the peer IPC blobs (link_peers),
   * build each rank's slab workload (configs.build_workload(rank, world)),
   * reduce per-rank partial seismograms in rank order (double) and cast to T,
   * gather halo-stripped slabs for checking.
@@ -19,21 +18,8 @@ import numpy as np
 from . import _lib
 
 
-def nccl_unique_id(group=None) -> bytes:
-    """ncclGetUniqueId on rank 0, broadcast to every rank of `group`."""
-    import torch.distributed as dist
-    buf = (C.c_ubyte * 128)()
-    if dist.get_rank(group) == 0:
-        rc = _lib.lib().fdw_nccl_unique_id(C.byref(buf))
-        if rc != 0:
-            raise RuntimeError("ncclGetUniqueId failed")
-    obj = [bytes(buf)]
-    dist.broadcast_object_list(obj, src=0, group=group)
-    return obj[0]
-
-
 def link_peers(solver, group=None) -> None:
-    """Peer transport (a slab Solver created with nccl_id None): all-gather
+    """Peer transport (a slab Solver, one process per GPU): all-gather
     every rank's IPC export blob and map the neighbours' levels and all sync
     blocks (fdw_peer_import).  Collective over `group`."""
     import torch.distributed as dist

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import sys
 import time
 from dataclasses import dataclass, field
 from typing import List, Optional
@@ -61,7 +62,7 @@ class InstabilityError(RuntimeError):  # kernel.hpp:48-62 instability_error
 
 
 class FdwError(RuntimeError):
-    """CUDA/NCCL-side failure reported through the C-ABI."""
+    """CUDA-side (or peer-transport) failure reported through the C-ABI."""
 
 
 def apply_boundary(f: np.ndarray, grid, spec: BoundarySpec) -> None:
@@ -129,8 +130,9 @@ class Solver:
     """fdwave::Solver<T> on the GPU.  T follows materials.velocity.dtype
     (float32 / float64).  Extra keyword-only knobs: device, variant
     (FDW_KERNEL_*), math (FDW_MATH_*), z_segments, and slab=(rank, world,
-    z_begin, z_end, nccl_id) for a Z-slab rank of a multi-GPU run (then the
-    field arrays are the rank's local padded slab)."""
+    z_begin, z_end) for a Z-slab rank of a multi-GPU run (then the field
+    arrays are the rank's local padded slab; link the ranks with peer_link /
+    dist.link_peers before stepping)."""
 
     def __init__(self, grid, materials, damping, boundary: BoundarySpec, time_axis, coeffs, *,
                  device: int = 0, variant: int = 0, math: int = 0, z_segments: int = 0,
@@ -169,10 +171,8 @@ class Solver:
         d.z_segments = int(z_segments)
         P = list(grid.padded_shape())
         if slab is not None:
-            rank, world, zb, ze, nccl_id = slab
+            rank, world, zb, ze = slab[:4]
             d.rank, d.world, d.z_begin, d.z_end = int(rank), int(world), int(zb), int(ze)
-            if nccl_id is not None:
-                C.memmove(d.nccl_id, bytes(nccl_id), 128)
             P[0] = int(ze - zb) + 2 * grid.halo
         self._shape = tuple(P[:grid.ndim]) if grid.ndim == 3 else (P[0], P[1])
         if vel.size != int(np.prod(self._shape)) or eta.size != vel.size:
@@ -197,6 +197,7 @@ class Solver:
         self._receiver_coordinates = []
         self._n_rec = 0
         self._verbose = False
+        self._loop_start = time.perf_counter()  # kernel.hpp:494 (reset by forward)
         self._snapshot_cap = 4 << 30
         self._prev = None
         self._curr = None
@@ -312,6 +313,32 @@ class Solver:
             self._download()
 
     def _advance(self, n: int, flags: int):
+        if self._verbose:  # check_health's progress line (kernel.hpp:456-466)
+            self._verbose_advance(n, flags & ~FDW_ADVANCE_ASYNC)
+            return
+        self._advance_raw(n, flags)
+
+    def _verbose_advance(self, n: int, flags: int):
+        """Steps in pieces that end at the health checks (step % 100 == 0 or
+        the last step); after each, the reference's line
+        "step s/N  t s  max|p| = m" on stderr, t since forward() began its loop."""
+        ci, total = 100, self._time.n_steps
+        s = self.step_index()
+        end = s + n
+        while s < end:
+            nxt = (s // ci + 1) * ci
+            if total > s:
+                nxt = min(nxt, total)
+            nxt = min(nxt, end)
+            self._advance_raw(nxt - s, flags)
+            s = nxt
+            if s % ci == 0 or s == total:
+                v = C.c_double()
+                _check(self._ctx, _lib.lib().fdw_max_abs(self._ctx, C.byref(v)), "fdw_max_abs")
+                sys.stderr.write("step %d/%d  %.3fs  max|p| = %.6e\n"
+                                 % (s, total, time.perf_counter() - self._loop_start, v.value))
+
+    def _advance_raw(self, n: int, flags: int):
         bad_step = C.c_uint64()
         bad_max = C.c_double()
         rc = _lib.lib().fdw_advance(self._ctx, n, flags, C.byref(bad_step), C.byref(bad_max))
@@ -368,6 +395,7 @@ class Solver:
             events = list(range((start // stride + 1) * stride, end + 1, stride))
         events.append(end)
         t0 = time.perf_counter()
+        self._loop_start = t0
         cur = start
         # steps and snapshot copies are queued without host syncs: each
         # snapshot streams out on the copy stream while later steps run
@@ -432,7 +460,7 @@ class Solver:
                 "variant": var.value & 0xFF, "z_segments": (var.value >> 8) & 0xFF,
                 "ctas_per_sm": var.value >> 16}
 
-    # -- peer transport (Z slabs over NVLink peer memory, no NCCL) --
+    # -- peer transport (Z slabs over NVLink peer memory) --
     def peer_export(self) -> bytes:
         """IPC handles of this rank's levels and sync block (fdw_peer_export)."""
         buf = (C.c_ubyte * _lib.FDW_PEER_BLOB_BYTES)()

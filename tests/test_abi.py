@@ -43,7 +43,7 @@ def test_desc_layout_matches_c():
     _lib.lib().fdw_desc_init(C.byref(d))
     assert d.abi_version == _lib.FDW_ABI_VERSION
     assert d.check_interval == 100 and d.world == 1 and d.dtype_bytes == 4
-    assert C.sizeof(_lib.fdw_desc) == 448
+    assert C.sizeof(_lib.fdw_desc) == 320
 
 
 @pytest.mark.parametrize("n,world", [(217, 1), (217, 2), (217, 8), (1600, 8), (19, 3)])
@@ -93,8 +93,16 @@ def test_create_rejects_bad_descriptors_without_touching_the_gpu():
     assert b"2*halo+2" in L.fdw_last_error(None)
 
 
+def test_library_needs_no_nccl():
+    """The halo exchange is peer memory, not NCCL: the library links no NCCL."""
+    import subprocess
+    r = subprocess.run(["readelf", "-d", _lib.LIB_PATH], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0
+    assert "nccl" not in r.stdout.lower(), r.stdout
+
+
 def test_library_then_torch_import_order():
-    """Loading the library before torch must not shadow torch's NCCL."""
+    """Loading the library before torch must not disturb torch's own NCCL."""
     import subprocess
     import sys
     code = ("from paper_2201_05278_b200 import _lib; _lib.lib(); import torch; "

@@ -116,11 +116,17 @@ def test_vd_rejects_shape_mismatch():
                w.axis, w.coeffs)
 
 
-def test_reference_test_kernel_cpp_on_the_drop_in():
+@pytest.mark.parametrize("devices", [None, "0,0"], ids=["one-gpu", "two-slabs"])
+def test_reference_test_kernel_cpp_on_the_drop_in(devices):
     """The reference's own tests/test_kernel.cpp, unmodified, compiled against
-    include/fdwave/kernel.hpp and linked to libfdwave_cuda.so (oracle/Makefile)."""
+    include/fdwave/kernel.hpp and linked to libfdwave_cuda.so (oracle/Makefile);
+    also with every 3D Solver split into two Z slabs (FDW_DEVICES=0,0, the
+    multi-GPU drop-in emulated on one GPU)."""
     exe = os.path.join(ROOT, "oracle", "_ref", "test_kernel_cuda")
     if not os.path.exists(exe):
         pytest.skip("oracle/_ref/test_kernel_cuda not built (needs the reference tree at build time)")
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    env = dict(os.environ)
+    if devices:
+        env["FDW_DEVICES"] = devices
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]

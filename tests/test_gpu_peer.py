@@ -1,10 +1,15 @@
-"""Peer transport (Z slabs, no NCCL) on one GPU: world 2 and 3 slabs driven
+"""Peer transport (Z slabs, no NCCL) on one GPU: world 2, 3 and 4 slabs driven
 from one process, one host thread per rank (fdw_peer_link).  Each step's TMA
-sweep stores its first / last R planes straight into the neighbours' levels,
-the point-source kernel mirrors targets in those planes, and one thread per
-rank signals / waits on step epochs in the sync blocks.  No kernel waits on a
-kernel of the same stream or on a grid that could be starved: the only waiters
-are 1-thread sync kernels, the sweeps never spin.
+sweep stores its first / last R planes straight into the neighbours' levels;
+its boundary CTAs wait for the neighbours' halo epoch and the last of them
+publishes the next one (a separate publish kernel when a point source writes
+into the halo planes after the sweep).
+
+All ranks share this box's one GPU, so the library runs the group
+HOST-ORDERED (fdw_peer_link sees the shared device): at every cross-rank point
+the rank threads meet at a host barrier and order their streams with events,
+so when a kernel checks a flag another launch sets, that launch has already
+completed -- no kernel ever waits on a concurrently running grid.
 
 The assembled wavefield must be bit-identical to the single-domain oracle; the
 seismogram equals the oracle's up to the split of each receiver's double sum at
@@ -28,13 +33,18 @@ from helpers import D, N, X, gpu_solver, oracle_solver, same, small_config
 from paper_2201_05278_b200.configs import build_workload
 h = 20.0
 shape = (41, 27, 25)   # extended Z = 51 planes: slabs 26/25 (world 2), 17/17/17 (world 3)
-cases = [(2, [(h * 20.5, h * 13.5, h * 12.5)]),                        # taps across the 2-slab face
-         (3, [(h * 11.5, h * 13.5, h * 12.5), (h * 28.5, h * 9.5, h * 10.5)])]
-for world, src in cases:
-    cfg = small_config(ndim=3, order=8, shape=shape, bc=[[N, D], [D, X], [D, N]], src=src, n_rec=9)
+# (world, sources, interior shape, Z segments): taps across the 2-slab face and
+# across both faces of 3 slabs (publish after the point-source kernel); 4 thin
+# slabs of 13 planes with automatic Z segments and the sources away from every
+# face (the sweep's last boundary CTA publishes)
+cases = [(2, [(h * 20.5, h * 13.5, h * 12.5)], shape, 3),
+         (3, [(h * 11.5, h * 13.5, h * 12.5), (h * 28.5, h * 9.5, h * 10.5)], shape, 3),
+         (4, [(h * 1.5, h * 13.5, h * 12.5), (h * 21.5, h * 9.5, h * 10.5)], (42, 27, 25), 0)]
+for world, src, shp, zseg in cases:
+    cfg = small_config(ndim=3, order=8, shape=shp, bc=[[N, D], [D, X], [D, N]], src=src, n_rec=9)
     for dt in (np.float32, np.float64):
         ws = [build_workload(cfg, dt, rank=r, world=world) for r in range(world)]
-        ss = [gpu_solver(w, slab=(*w.slab, None), z_segments=3) for w in ws]
+        ss = [gpu_solver(w, slab=w.slab, z_segments=zseg) for w in ws]
         for s, w in zip(ss, ws):
             assert s.layout()["variant"] == 3
             s.set_sources(w.sources, w.wavelet)
@@ -74,7 +84,7 @@ def test_peer_transport_slabs_bit_exact_on_one_gpu():
     r = subprocess.run([sys.executable, "-c", CHILD.format(here=HERE)], capture_output=True, text=True,
                        timeout=900, cwd=os.path.dirname(HERE))
     assert r.returncode == 0 and "peer all ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
-    assert r.stdout.count("peer ok") == 4, r.stdout
+    assert r.stdout.count("peer ok") == 6, r.stdout
 
 
 CHILD2 = r'''
@@ -108,7 +118,7 @@ field = rng.standard_normal(w.velocity.shape).astype(np.float32)
 amp = list(np.sin(np.arange(w.axis.n_steps + 1) * 0.3))
 world = 2
 ws = [build_workload(cfg, np.float32, rank=r, world=world) for r in range(world)]
-ss = [gpu_solver(x, slab=(*x.slab, None)) for x in ws]
+ss = [gpu_solver(x, slab=x.slab) for x in ws]
 for s, x in zip(ss, ws):
     s.set_sources(x.sources, x.wavelet)
     zb, ze = x.slab[2], x.slab[3]
@@ -146,7 +156,7 @@ for r in range(world):
     x = build_workload(cfg, np.float32, rank=r, world=world)
     x.axis.dt, x.axis.n_steps, x.wavelet = w.axis.dt, 1000, w.wavelet
     ws.append(x)
-ss = [gpu_solver(x, slab=(*x.slab, None)) for x in ws]
+ss = [gpu_solver(x, slab=x.slab) for x in ws]
 for s, x in zip(ss, ws):
     s.set_sources(x.sources, x.wavelet)
 for s in ss:

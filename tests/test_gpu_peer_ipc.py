@@ -26,7 +26,7 @@ def _worker(rank, world, port, q):
     try:
         cfg = small_config(ndim=3, order=8, shape=(30, 21, 19))
         w = build_workload(cfg, np.float32, rank=rank, world=world)
-        s = gpu_solver(w, slab=(*w.slab, None))
+        s = gpu_solver(w, slab=w.slab)
         blob = s.peer_export()
         assert len(blob) == 512
         errs = []
