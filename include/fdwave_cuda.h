@@ -250,6 +250,24 @@ fdw_status fdw_peer_import(fdw_solver* ctx, const unsigned char* blobs, int32_t 
 /* One process driving every rank (one thread per context): all[r] = rank r. */
 fdw_status fdw_peer_link(fdw_solver* ctx, fdw_solver* const* all, int32_t world);
 
+/* Debug: with FDW_GUARD_CHECK=1 set when the context is created, every field
+ * allocation carries a patterned guard zone after its end.  Counts the guard
+ * words that changed, plus every non-zero element OUTSIDE the padded box of
+ * the two wavefield levels (row / column slack, spare plane), where no kernel
+ * may write.  (Out-of-bounds store detection of our own: compute-sanitizer is
+ * not available on the GPU pool this was built on.) */
+fdw_status fdw_debug_check_guards(fdw_solver* ctx, uint64_t* n_bad);
+
+/* Profiling hook: emulated neighbours for a slab context on ONE GPU.  The
+ * halo planes this rank stores go to scratch levels on its own GPU, and the
+ * neighbours' halo epochs and health posts are pre-satisfied, so the step runs
+ * the complete multi-GPU path (boundary-first Z segments, in-sweep epoch waits
+ * and publish, fused halo stores, cross-rank health reduction) without
+ * another rank; only the NVLink transfer itself is absent.  Instead of
+ * fdw_peer_import / fdw_peer_link.  The wavefield is not a valid slab
+ * solution (its ghost planes are never refreshed): for timing only. */
+fdw_status fdw_peer_loopback(fdw_solver* ctx);
+
 /* ---- host-only helpers (no GPU needed) ---- */
 
 /* Z-slab split of n_ext planes over `world` ranks: [*z_begin, *z_end). */

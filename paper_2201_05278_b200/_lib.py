@@ -85,6 +85,8 @@ _SIGS = {
     "fdw_peer_export": (C.c_int, [_P, _P]),
     "fdw_peer_import": (C.c_int, [_P, _P, C.c_int32]),
     "fdw_peer_link": (C.c_int, [_P, _P, C.c_int32]),
+    "fdw_peer_loopback": (C.c_int, [_P]),
+    "fdw_debug_check_guards": (C.c_int, [_P, _U64P]),
 }
 
 FDW_PEER_BLOB_BYTES = 512

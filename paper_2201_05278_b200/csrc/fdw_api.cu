@@ -26,6 +26,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
 #include <unistd.h>
 
 #include "../../include/fdwave_cuda.h"
@@ -43,6 +44,14 @@ struct ProfileSink {
 };
 
 }  // namespace
+
+// NVTX ranges (header-only NVTX3, no link dependency) around the host calls
+// that enqueue device work, so an nsys / ncu timeline groups the kernels by
+// chunk, health check, upload and snapshot.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // FDW_DEBUG_TIMING=1: host-side phase timings of the setup/teardown calls
 struct PhaseTimer {
@@ -206,12 +215,23 @@ struct fdw_solver {
     bool ipc_same_device = false;  // an IPC-imported neighbour shares this GPU (cannot step)
     struct HostGroup* group = nullptr;  // host-ordered ranks (fdw_peer_link with a shared GPU)
     bool no_pdl = false;           // FDW_NO_PDL at create time
+    int prio_hi = 0, prio_lo = 0;  // launch priorities: step chain / side-stream receivers (FDW_NO_PRIO: equal)
     bool tail_pdl_aware = false;   // last kernel of the previous step on `stream` is PDL-aware
     fdw::PeerSync* psync = nullptr;                        // own sync block (cudaMalloc, IPC-exportable)
     fdw::PeerSync* peer_sync[fdw::PEER_MAX_WORLD] = {};    // every rank's block, mapped
     void* peer_lvl[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [lower, upper][level], mapped
     long long peer_delta[2] = {0, 0};                      // neighbour element = local element + delta
     std::vector<void*> ipc_mapped;                         // cudaIpcCloseMemHandle on destroy
+    // FDW_GUARD_CHECK=1: a patterned zone after each field allocation
+    static constexpr size_t GUARD = 1 << 16;
+    size_t guard_bytes = 0;
+    // fdw_peer_loopback (profiling): emulated neighbours on this GPU
+    bool loopback = false;
+    // timing experiments (tools/peer_overhead.py), read at create: FDW_DBG_NO_SEGROT,
+    // FDW_DBG_NO_HALO_STORE (loopback only), FDW_DBG_FENCE_ALL
+    bool dbg_no_rot = false, dbg_no_store = false, dbg_fence_all = false;
+    void* loop_lvl[2] = {nullptr, nullptr};
+    fdw::PeerSync* loop_sync = nullptr;
 };
 
 namespace {
@@ -570,7 +590,9 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
             if ((a.peer_lo && zs < R) || (a.peer_hi && ze > nz - R)) ++nseg;
         }
         a.n_bnd = nseg * grid.x * grid.y;
-        a.seg_rot = S - 1;
+        a.seg_rot = c->dbg_no_rot ? 0 : S - 1;
+        a.halo_store = c->loopback && c->dbg_no_store ? 0 : 1;
+        a.fence_all = c->dbg_fence_all ? 1 : 0;
     }
     const int col_base = (int)(c->base + c->R);
     const int smem = tma_smem<T>(c->R, c->vd);
@@ -579,16 +601,25 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
     const CUtensorMap& g2 = c->tm_g[2];
     // programmatic dependent launch: the sweep's prologue (mbarrier setup,
     // eta-range load) overlaps the predecessor's tail; it waits in-kernel
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    // the time-step chain runs at high priority: a receiver kernel on the
+    // side stream only takes the SM slots the sweep's last wave leaves free
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (c->prio_hi != c->prio_lo) {
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na++].val.priority = c->prio_hi;
+    }
+    if (c->pdl_sweep) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = st;
     cfg.attrs = attr;
-    cfg.numAttrs = c->pdl_sweep ? 1 : 0;
+    cfg.numAttrs = na;
     auto go = [&](auto kern) {
         // an error is left for the caller's CHECK_LAUNCH (cudaGetLastError)
         (void)cudaLaunchKernelEx(&cfg, kern, a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);
@@ -1036,15 +1067,22 @@ fdw_status launch_inject_t(fdw_solver* c, int dst, int k, int t0 = 0, int cnt = 
         pm.lo_end = c->origin + (long long)c->R * c->plane;
         pm.hi_begin = c->origin + (c->nzl - c->R) * c->plane;
     }
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (c->prio_hi != c->prio_lo) {
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na++].val.priority = c->prio_hi;
+    }
+    if (pdl) {  // PDL: setup-time loads overlap the sweep's tail (inject_kernel)
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)((cnt + tb - 1) / tb));
     cfg.blockDim = dim3(tb);
     cfg.stream = st;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;  // PDL: setup-time loads overlap the sweep's tail (inject_kernel)
+    cfg.numAttrs = na;
     (void)cudaLaunchKernelEx(&cfg, fdw::inject_kernel<T, true>, static_cast<T*>(c->lvl[dst]),
                              static_cast<const T*>(c->c2dt2), static_cast<const T*>(c->eta), c->d.dt,
                              static_cast<const long long*>(c->d_tgt + t0),
@@ -1257,7 +1295,7 @@ void peer_leave(fdw_solver* c) {
         }
         return;
     }
-    if (c->ipc_same_device) return;  // such a context never stepped (peers_usable)
+    if (c->ipc_same_device || c->loopback) return;  // never stepped (peers_usable) / no real peers
     fdw::peer_quiesce<<<1, 32, 0, c->stream>>>(peer_args(c), 5000000000ull);
     cudaStreamSynchronize(c->stream);
     cudaGetLastError();
@@ -1278,10 +1316,19 @@ fdw_status launch_peer_health(fdw_solver* c, int honor_abort) {
 template <typename T>
 fdw_status launch_receivers_t(fdw_solver* c, int lv, int row_add, cudaStream_t st) {
     if (c->n_rec == 0 || !c->d_seis) return FDW_OK;
-    fdw::receivers_kernel<T><<<(c->n_rec + fdw::REC_WARPS - 1) / fdw::REC_WARPS, 32 * fdw::REC_WARPS, 0,
-                               st>>>(
-        static_cast<const T*>(c->lvl[lv]), c->d_rec_idx, c->d_rec_off, c->d_rec_w, c->d_seis, c->n_rec,
-        c->seis_rows, row_add, c->ctrl);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = c->prio_lo;  // below the step chain (launch_tma)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((c->n_rec + fdw::REC_WARPS - 1) / fdw::REC_WARPS));
+    cfg.blockDim = dim3(32 * fdw::REC_WARPS);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = c->prio_hi != c->prio_lo ? 1 : 0;
+    (void)cudaLaunchKernelEx(&cfg, fdw::receivers_kernel<T>, static_cast<const T*>(c->lvl[lv]),
+                             static_cast<const long long*>(c->d_rec_idx), static_cast<const unsigned int*>(c->d_rec_off),
+                             static_cast<const double*>(c->d_rec_w), c->d_seis, c->n_rec, c->seis_rows, row_add,
+                             static_cast<const fdw::Ctrl*>(c->ctrl));
     CHECK_LAUNCH();
     return FDW_OK;
 }
@@ -1369,6 +1416,7 @@ fdw_status launch_health_t(fdw_solver* c, int lv, int honor_abort) {
 }
 
 fdw_status launch_health(fdw_solver* c, int lv, int honor_abort) {
+    NvtxRange nv("fdw health check");
     return c->tsize == 4 ? launch_health_t<float>(c, lv, honor_abort) : launch_health_t<double>(c, lv, honor_abort);
 }
 
@@ -1627,6 +1675,7 @@ fdw_status enqueue_chunk(fdw_solver* c, unsigned long long L, int cur0, bool che
 }
 
 fdw_status run_chunk(fdw_solver* c, unsigned long long L, bool check, bool record) {
+    NvtxRange nv(check ? "fdw chunk + health" : "fdw chunk");
     const int cur0 = c->cur;
     const bool first_virt = virtual_step(c, c->gstate[cur0]);
     const bool rest_virt = virtual_step(c, 0);
@@ -2072,7 +2121,72 @@ fdw_status fdw_peer_link(fdw_solver* c, fdw_solver* const* all, int32_t world) {
     return FDW_OK;
 }
 
+fdw_status fdw_debug_check_guards(fdw_solver* c, uint64_t* n_bad) {
+    fdw_status s = enter(c);
+    if (s) return s;
+    if (!n_bad) return fail(c, FDW_EINVAL, "null output");
+    if (!c->guard_bytes) return fail(c, FDW_ESTATE, "guards are off: create the context with FDW_GUARD_CHECK=1");
+    CU(cudaStreamSynchronize(c->side));
+    unsigned long long* d_bad = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&d_bad), sizeof(*d_bad), c->stream));
+    CU(cudaMemsetAsync(d_bad, 0, sizeof(*d_bad), c->stream));
+    const size_t body = c->level_elems * c->tsize;
+    const long long nrows = c->ndim == 3 ? c->P[1] : c->P[0];
+    const long long ncols = c->ndim == 3 ? c->P[2] : c->P[1];
+    const long long nplanes = c->ndim == 3 ? c->Lz : 1;
+    int k = 0;
+    for (void* p : {c->lvl[0], c->lvl[1], c->c2dt2, c->eta}) {
+        const int slack = k++ < 2;  // levels: nothing may land outside the padded box
+        fdw::guard_scan<<<c->sm_count * 4, 256, 0, c->stream>>>(
+            static_cast<const unsigned int*>(p), (body + c->guard_bytes) / 4, body / 4, slack, c->ld, c->plane,
+            c->base, nrows, ncols, nplanes, c->tsize, d_bad);
+        CHECK_LAUNCH();
+    }
+    unsigned long long h = 0;
+    CU(cudaMemcpyAsync(&h, d_bad, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaFreeAsync(d_bad, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    *n_bad = h;
+    return FDW_OK;
+}
+
+fdw_status fdw_peer_loopback(fdw_solver* c) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (!c->peer_mode) return fail(c, FDW_EINVAL, "not a peer-transport slab context");
+    if (c->peers_ready) return fail(c, FDW_ESTATE, "peers already linked");
+    const size_t bytes = c->level_elems * c->tsize;
+    for (int l = 0; l < 2; ++l) CU(cudaMalloc(&c->loop_lvl[l], bytes));
+    CU(cudaMalloc(reinterpret_cast<void**>(&c->loop_sync), sizeof(fdw::PeerSync)));
+    CU(cudaMemset(c->loop_sync, 0, sizeof(fdw::PeerSync)));
+    // the neighbours' epochs and health posts are already far ahead, their
+    // inbox values neutral (no non-finite index, max 0, kind 0)
+    fdw::PeerSync h{};
+    CU(cudaMemcpy(&h, c->psync, sizeof(h), cudaMemcpyDeviceToHost));
+    const int r = c->d.rank;
+    for (int q = 0; q < c->d.world; ++q) {
+        if (q == r) continue;
+        h.halo_flag[q] = h.health_flag[q] = 1ull << 62;
+        for (int k = 0; k < 2; ++k) {
+            h.in_idx[k][q] = ~0ull;
+            h.in_max[k][q] = 0ull;
+            h.in_kind[k][q] = 0u;
+        }
+        c->peer_sync[q] = c->loop_sync;  // this rank's posts and publishes land in scratch
+    }
+    CU(cudaMemcpy(c->psync, &h, sizeof(h), cudaMemcpyHostToDevice));
+    for (int side = 0; side < 2; ++side) {
+        const bool has = side == 0 ? r > 0 : r < c->d.world - 1;
+        for (int l = 0; l < 2; ++l) c->peer_lvl[side][l] = has ? c->loop_lvl[l] : nullptr;
+        c->peer_delta[side] = 0;  // halo planes land at the same offsets of the scratch level
+    }
+    c->loopback = true;
+    c->peers_ready = true;
+    return FDW_OK;
+}
+
 fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
+    NvtxRange nv("fdw_create");
     fdw_solver* c = nullptr;
     if (!dp || !out) return fail(nullptr, FDW_EINVAL, "null descriptor");
     const fdw_desc& d = *dp;
@@ -2197,13 +2311,29 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
     }
     c->peer_mode = c->ndim == 3 && d.world > 1;
     c->no_pdl = std::getenv("FDW_NO_PDL") != nullptr;
+    c->dbg_no_rot = std::getenv("FDW_DBG_NO_SEGROT") != nullptr;
+    c->dbg_no_store = std::getenv("FDW_DBG_NO_HALO_STORE") != nullptr;
+    c->dbg_fence_all = std::getenv("FDW_DBG_FENCE_ALL") != nullptr;
+    if (!std::getenv("FDW_NO_PRIO")) {
+        int lo = 0, hi = 0;
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess) {
+            c->prio_lo = lo;
+            c->prio_hi = hi;
+        }
+        cudaGetLastError();
+    }
+    c->guard_bytes = std::getenv("FDW_GUARD_CHECK") ? fdw_solver::GUARD : 0;
     for (void** p : {&c->lvl[0], &c->lvl[1], &c->c2dt2, &c->eta}) {
         // peer transport: the levels are mapped by the neighbours (cudaIpc
         // needs cudaMalloc memory, not the stream-ordered pool)
         const bool ipc = c->peer_mode && (p == &c->lvl[0] || p == &c->lvl[1]);
-        if (!ck(ipc ? cudaMalloc(p, bytes) : cudaMallocAsync(p, bytes, c->stream), "cudaMalloc(level)"))
+        const size_t nb = bytes + c->guard_bytes;
+        if (!ck(ipc ? cudaMalloc(p, nb) : cudaMallocAsync(p, nb, c->stream), "cudaMalloc(level)"))
             return bail(FDW_ENOMEM);
         if (!ck(cudaMemsetAsync(*p, 0, bytes, c->stream), "memset")) return bail(FDW_ECUDA);
+        if (c->guard_bytes &&
+            !ck(cudaMemsetAsync(static_cast<char*>(*p) + bytes, 0xA5, c->guard_bytes, c->stream), "memset"))
+            return bail(FDW_ECUDA);
     }
     if (c->peer_mode) {
         if (d.world > fdw::PEER_MAX_WORLD) {
@@ -2297,6 +2427,7 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
 }
 
 fdw_status fdw_destroy(fdw_solver* c) {
+    NvtxRange nv("fdw_destroy");
     if (!c) return FDW_OK;
     PhaseTimer pt("fdw_destroy");
     auto lap = [&](const char* w) { pt.lap(w); };
@@ -2321,6 +2452,8 @@ fdw_status fdw_destroy(fdw_solver* c) {
     lap("graphs");
     peer_leave(c);
     for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
+    for (void* p : {c->loop_lvl[0], c->loop_lvl[1], (void*)c->loop_sync})
+        if (p) cudaFree(p);
     if (c->peer_mode) {
         if (c->stream) cudaStreamSynchronize(c->stream);
         for (void* p : {c->lvl[0], c->lvl[1], (void*)c->psync})
@@ -2364,6 +2497,7 @@ fdw_status fdw_set_stream(fdw_solver* c, void* stream) {
 }
 
 fdw_status fdw_set_medium(fdw_solver* c, const void* velocity, const void* eta, int on_device) {
+    NvtxRange nv("fdw_set_medium");
     fdw_status s = enter(c);
     if (s) return s;
     if (!velocity || !eta) return fail(c, FDW_EINVAL, "velocity and eta are required");
@@ -2615,6 +2749,7 @@ fdw_status fdw_set_receivers(fdw_solver* c, uint64_t n_points, const uint64_t* o
 }
 
 fdw_status fdw_set_levels(fdw_solver* c, const void* prev, const void* curr) {
+    NvtxRange nv("fdw_set_levels");
     fdw_status s = enter(c);
     if (s) return s;
     if (prev && (s = copy_host_to_level(c, c->lvl[1 - c->cur], prev, 0))) return s;
@@ -2636,6 +2771,7 @@ fdw_status fdw_zero_levels(fdw_solver* c) {
 }
 
 fdw_status fdw_get_levels(fdw_solver* c, void* prev, void* curr) {
+    NvtxRange nv("fdw_get_levels");
     fdw_status s = enter(c);
     if (s) return s;
     if (prev && (s = settle_ghosts(c, 1 - c->cur))) return s;
@@ -2725,6 +2861,7 @@ void CUDART_CB snap_host_copy(void* p) {
 }  // namespace
 
 fdw_status fdw_snapshot_async(fdw_solver* c, void* out) {
+    NvtxRange nv("fdw_snapshot_async");
     fdw_status s = prologue(c);
     if (s) return s;
     if (!out) return fail(c, FDW_EINVAL, "null snapshot destination");

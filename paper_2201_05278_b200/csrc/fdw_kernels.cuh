@@ -270,6 +270,8 @@ struct SweepArgs {
     PeerArgs peer;
     unsigned int n_bnd;
     int publish;
+    int halo_store;  // 0: skip the halo stores (fdw_peer_loopback timing experiments only)
+    int fence_all;   // 1: every thread fences its stores (A/B of the one-fence-per-CTA release)
     T negz;  // -0 (runtime value for the packed exact products)
     const Ctrl* ctrl;
 };
@@ -937,7 +939,7 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
     // re-reads its own just-written outputs; outside the plane loop, so the
     // hot loop's registers are untouched), performed system-wide before the
     // grid ends
-    if ((plo || phi) && xin) {
+    if ((plo || phi) && xin && a.halo_store) {
         auto copy_plane = [&](T* peer, long long delta, int z) {
             const T* o = a.out + col0 + (long long)z * plane;
             T* po = peer + (col0 + (long long)z * plane + delta);
@@ -954,12 +956,17 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
             for (int z = max(zs, nz - R); z < ze; ++z) copy_plane(a.peer_hi, a.peer_hi_delta, z);
     }
     if (plo || phi) {
-        // the last boundary CTA of the step publishes the next epoch
-        __threadfence_system();
+        // release: the CTA's halo stores (ordered before thread 0 by the
+        // barrier, fence cumulativity) are made visible system-wide by one
+        // fence; the last boundary CTA of the step publishes the next epoch
+        if (a.fence_all) __threadfence_system();
         __syncthreads();
-        if (tid == 0 && a.publish && atomicAdd(&a.peer.self->bnd_done, 1u) == a.n_bnd - 1) {
-            a.peer.self->bnd_done = 0u;
-            peer_publish(a.peer);
+        if (tid == 0) {
+            __threadfence_system();
+            if (a.publish && atomicAdd(&a.peer.self->bnd_done, 1u) == a.n_bnd - 1) {
+                a.peer.self->bnd_done = 0u;
+                peer_publish(a.peer);
+            }
         }
     }
 }
@@ -2426,6 +2433,29 @@ __global__ void __launch_bounds__(256) health_scan_ext(const T* __restrict__ u, 
         atomicMax(&ctrl->max_bits, (unsigned long long)__double_as_longlong(md));
         if (bad != ~0ull) atomicMin(&ctrl->bad_idx, bad);
     }
+}
+
+// Debug guard check (FDW_GUARD_CHECK=1, fdw_debug_check_guards): the bytes
+// past each allocation hold a pattern, and in a wavefield level every element
+// outside the padded box (row / column slack, the spare plane) must still be
+// zero -- no kernel may write there.  Counts the violations.
+__global__ void guard_scan(const unsigned int* __restrict__ a, unsigned long long n_words,
+                           unsigned long long body_words, int check_slack, long long ld, long long plane,
+                           long long base, long long nrows, long long ncols, long long nplanes, int tsize,
+                           unsigned long long* bad) {
+    unsigned long long cnt = 0;
+    for (unsigned long long w = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; w < n_words;
+         w += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned int v = a[w];
+        if (w >= body_words) {
+            cnt += v != 0xA5A5A5A5u;
+        } else if (check_slack && v != 0u) {
+            const long long e = (long long)(w * 4 / tsize);
+            const long long p = e / plane, rem = e % plane, r = rem / ld, col = rem % ld;
+            cnt += !(p < nplanes && r < nrows && col >= base && col < base + ncols);
+        }
+    }
+    if (cnt) atomicAdd(bad, cnt);
 }
 
 __global__ void health_reset(Ctrl* ctrl, int honor_abort) {

@@ -478,6 +478,16 @@ class Solver:
         arr = (C.c_void_p * len(solvers))(*[s._ctx.value for s in solvers])
         _check(self._ctx, _lib.lib().fdw_peer_link(self._ctx, arr, len(solvers)), "fdw_peer_link")
 
+    def debug_check_guards(self) -> int:
+        """Guard / slack violations (context created with FDW_GUARD_CHECK=1)."""
+        v = C.c_uint64()
+        _check(self._ctx, _lib.lib().fdw_debug_check_guards(self._ctx, C.byref(v)), "fdw_debug_check_guards")
+        return int(v.value)
+
+    def peer_loopback(self) -> None:
+        """Profiling: emulated neighbours on this GPU (fdw_peer_loopback)."""
+        _check(self._ctx, _lib.lib().fdw_peer_loopback(self._ctx), "fdw_peer_loopback")
+
     def set_stream(self, stream_ptr: int):
         _check(self._ctx, _lib.lib().fdw_set_stream(self._ctx, C.c_void_p(stream_ptr)), "fdw_set_stream")
 
