@@ -55,7 +55,7 @@ def parse():
     p.add_argument("--math", default="exact", choices=["exact", "fma"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--cpu-seconds", type=float, default=24.0)
     return p.parse_args()
 
 
@@ -136,15 +136,23 @@ class ClockSampler:
 
 
 def traffic_for(workload):
-    """dram bytes (read+write) per sweep launch from the committed ncu capture."""
+    """DRAM bytes (read + write) per sweep launch from the committed ncu capture
+    (profiles/ncu_traffic.json).  Valid only for the kernel source it was
+    captured from: the capture records the SHA-256 of csrc/fdw_kernels.cuh, and
+    a changed source reports null instead of a stale number."""
+    import hashlib
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(workload)
-    except Exception:
-        return None
+            d = json.load(f)
+        with open(os.path.join(ROOT, "paper_2201_05278_b200", "csrc", "fdw_kernels.cuh"), "rb") as f:
+            cur = hashlib.sha256(f.read()).hexdigest()
+        if d.get("kernels_sha256") != cur:
+            return None, "stale: fdw_kernels.cuh changed since the ncu capture"
+        return d.get(workload), d.get("source")
+    except Exception as e:
+        return None, f"unavailable: {e}"
 
 
-# --------------------------------------------------------------------------
 class TorchEnv:
     """One process per GPU under torchrun (RANK / LOCAL_RANK / WORLD_SIZE):
     torch.distributed carries only control traffic; the ranks' levels and
@@ -410,15 +418,29 @@ def bench_rank(args, env):
     # at step n_steps.  (A field that is still mostly zero draws less power
     # and runs the sweep at a higher clock: about 10% faster on B200 under the
     # power cap, so timing kernels from rest would flatter the roofline.)
+    # the states at n_steps / 2 and n_steps seed the CPU baseline's samples
+    # (the reference's CPU rate changes over a run: subnormal arithmetic in the
+    # numerical precursor ahead of the wavefront slows the middle of the run)
+    cpu_states = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu_states = {"end": (solver.previous_level().copy(), solver.current_level().copy())}
+        solver._host_view = False
     prof = solver.profile_steps(min(200, n_steps))
     sweep_ms = prof[0]
+    if cpu_states is not None:
+        one_half = n_steps // 2
+        solver.reset_state()
+        solver.refresh_boundary()
+        solver.advance_raw(one_half)
+        cpu_states["mid"] = (solver.previous_level().copy(), solver.current_level().copy())
+        solver._host_view = False
     hbm, hbm_src = peaks()
     achieved = local_pts * BYTES_PER_POINT / (sweep_ms * 1e-3) / 1e9
     step_ms_dev = ms_per_step / n_steps
     # whole-step figure: the same algorithmic bytes over the timed step time
     # (sweep + inject + receivers + health + launch gaps, in the CUDA graph)
     step_achieved = local_pts * BYTES_PER_POINT / (step_ms_dev * 1e-3) / 1e9
-    tr = traffic_for(wname)
+    tr, tr_src = traffic_for(wname)
 
     # e2e: the public API with host buffers (pinned), H2D + D2H inside the region
     e2e = None
@@ -473,7 +495,7 @@ def bench_rank(args, env):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(cfg, args.cpu_seconds)
+        cpu = cpu_baseline(cfg, args.cpu_seconds, cpu_states, wname, n_steps)
 
     env.close()
     if rank != 0:
@@ -497,7 +519,8 @@ def bench_rank(args, env):
             "vs_baseline_ref": "BASELINE.md 3D SO8 V100 OpenMP offload 63.12 s -> 5.58 Gpts/s (PAPER.md:93)",
         },
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4), "traffic": tr, "peak_source": hbm_src,
+                     "frac": round(achieved / hbm, 4), "traffic": tr, "traffic_source": tr_src,
+                     "peak_source": hbm_src,
                      "kernel": "sweep (stencil3d/2d)", "bytes_per_point": BYTES_PER_POINT,
                      "state": "developed wavefield (kernels timed after the timed forwards, from step n_steps)",
                      "step_achieved": round(step_achieved, 1), "step_frac": round(step_achieved / hbm, 4),
@@ -516,28 +539,55 @@ def bench_rank(args, env):
     return line
 
 
-def cpu_baseline(cfg, seconds):
+def cpu_baseline(cfg, seconds, states=None, wname=None, n_steps=None):
     """The reference's own Solver<float> (oracle/_ref, compiled in place from the
-    reference headers) on this host's cores: bounded sample of the same workload."""
+    reference headers) on this host's cores: bounded samples of the same
+    workload.  The CPU's rate is not constant over a run (a field of exact
+    zeros is fast; subnormals in the numerical precursor ahead of the
+    wavefront are slow), so the value samples three points of the run --
+    from rest, and from the GPU's states at n/2 and n loaded into the reference
+    Solver's levels -- and reports points x steps / seconds over all three.
+    The full-length run of the fixture generator is reported beside it."""
     try:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
         if O.rlib() is None:
             raise RuntimeError("no reference library")
-        kind = "reference"
         t0 = time.time()
         run = O.RefRun(cfg, np.float32, threads=0)
         setup = time.time() - t0
         pts = int(np.prod(run.extended))
-        probe = run.time_steps(1)
-        k = max(1, min(60, int(seconds / max(probe, 1e-6)) - 1))
-        el = probe + run.time_steps(k)
-        n = k + 1
         cores = int(O.rlib().ref_max_threads())
-        return {"value": round(pts * n / el / 1e9, 4), "unit": UNIT, "cores": cores, "kind": kind,
-                "sample": f"first {n} time steps of {cfg.name} ({pts} ext pts) from rest, reference "
-                          f"Solver<float> Backend::Parallel, {el:.1f} s loop (setup {setup:.1f} s excluded)",
-                "cpu_model": _cpu_model()}
+        parts = ["rest"] + ([k for k in ("mid", "end") if k in states] if states else [])
+        per = seconds / len(parts)
+        run.time_steps(1)  # OpenMP pool and first-touch warm-up, untimed
+        samples = {}
+        for name in parts:
+            if name != "rest":
+                run.set_levels(*states[name])
+            probe = run.time_steps(1)
+            k = max(1, min(60, int(per / max(probe, 1e-6)) - 1))
+            el = probe + run.time_steps(k)
+            samples[name] = (k + 1, el)
+        n_all = sum(v[0] for v in samples.values())
+        t_all = sum(v[1] for v in samples.values())
+        at = {"rest": "step 0", "mid": f"step {n_steps // 2}" if n_steps else "mid-run",
+              "end": f"step {n_steps}" if n_steps else "end"}
+        out = {"value": round(pts * n_all / t_all / 1e9, 4), "unit": UNIT, "cores": cores, "kind": "reference",
+               "sample": f"{n_all} time steps of {cfg.name} ({pts} ext pts) in {len(samples)} runs of ~{per:.0f} s from "
+                         + ", ".join(f"{at[k]} ({v[0]} steps, {v[1]:.1f} s)" for k, v in samples.items())
+                         + " (states after step 0 are the GPU's, loaded into the reference Solver's levels); "
+                           f"reference Solver<float> Backend::Parallel; setup {setup:.1f} s excluded",
+               "per_state_gpts": {k: round(pts * v[0] / v[1] / 1e9, 4) for k, v in samples.items()},
+               "cpu_model": _cpu_model()}
+        full = os.path.join(ROOT, "tests", "golden", f"full_{(wname or '').lower()}.npz")
+        if os.path.exists(full):
+            import json as _json
+            m = _json.loads(str(np.load(full)["meta"]))
+            out["full_run"] = {"gpts": round(m["gpts_per_s"], 4), "seconds": round(m["seconds"], 1),
+                               "steps": m["n_steps"], "threads": m["threads"],
+                               "where": "build container (not this host), oracle/gen_fullsize.py"}
+        return out
     except Exception as e:  # keep the GPU line valid
         return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                 "sample": f"unavailable: {e}"}

@@ -355,6 +355,18 @@ class RefRun:
             return {"unstable": (int(bs.value), float(bm.value))}
         return {"seismogram": seis[: (self.n_steps + 1) * self.n_rec], "final": final, "seconds": secs.value}
 
+    def set_levels(self, prev, curr):
+        """Overwrites the reference Solver's levels (current_level() /
+        previous_level() are mutable references, kernel.hpp:217-218), e.g. with
+        a developed wavefield for a representative CPU timing sample."""
+        L = rlib()
+        for which, a in ((0, prev), (1, curr)):
+            a = np.ascontiguousarray(a, self.dtype)
+            n = int(np.prod(self.padded))
+            if a.size != n:
+                raise ValueError("level shape does not match the padded grid")
+            C.memmove(L.ref_level(self.h, which), a.ctypes.data, a.nbytes)
+
     def time_steps(self, n):
         secs = C.c_double()
         rc = rlib().ref_time_steps(self.h, n, C.byref(secs))
