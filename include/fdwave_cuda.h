@@ -211,7 +211,7 @@ fdw_status fdw_launch_count(const fdw_solver* ctx, uint64_t* n);
 
 /* Introspection: device layout of one level (elements): row pitch, plane pitch,
  * column base, stored planes, selected kernel variant | z_segments << 8 |
- * resident CTAs per SM << 16. */
+ * resident CTAs per SM << 16 | TMA planes in flight (split rings, 0: one) << 24. */
 fdw_status fdw_layout(const fdw_solver* ctx, uint64_t* ld, uint64_t* plane,
                       uint64_t* base, uint64_t* planes, int32_t* variant);
 

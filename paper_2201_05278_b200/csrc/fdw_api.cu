@@ -149,6 +149,7 @@ struct fdw_solver {
     int bx = 16;
     int occupancy = 0;
     int tma_minb = 3;
+    int tma_pd = 0;  // > 0: split-ring TMA sweep with that many planes in flight
 
     std::map<std::tuple<unsigned long long, int, int, int>, cudaGraphExec_t> graphs;
     std::map<std::tuple<unsigned long long, int, int, int>, unsigned long long> graph_kernels;
@@ -517,8 +518,17 @@ const void* tma_fn() {
     return (const void*)fdw::sweep3d_tma<T, R, TMA_BX, EX, MINB>;
 }
 
+constexpr int TMA_PD = 2;  // split-ring prefetch depth (FDW_TMA_PD=2)
+
 template <typename T>
-int tma_smem(int R, bool vd = false) {
+int tma_smem(int R, bool vd = false, int pd = 0) {
+    if (pd > 0 && !vd) {
+        switch (R) {
+            case 1: return fdw::TmaShape<T, 1, TMA_BX, 3, TMA_PD>::SMEM;
+            case 2: return fdw::TmaShape<T, 2, TMA_BX, 3, TMA_PD>::SMEM;
+            default: return fdw::TmaShape<T, 4, TMA_BX, 3, TMA_PD>::SMEM;
+        }
+    }
     if (vd) {
         switch (R) {
             case 1: return fdw::TmaShape<T, 1, TMA_BX, 6>::SMEM;
@@ -548,7 +558,17 @@ const void* tma_vd_kernel(int R, bool ex) {
 
 // minb: 2 or 3 resident CTAs requested from ptxas (register cap 128 / 80)
 template <typename T>
-const void* tma_kernel(int R, bool ex, int minb) {
+const void* tma_kernel(int R, bool ex, int minb, int pd = 0) {
+    if (pd > 0) {  // split rings: 3 CTAs/SM only
+#define TKP(RR) \
+    if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 3, false, TMA_PD> \
+                           : (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, false, 3, false, TMA_PD>;
+        TKP(1)
+        TKP(2)
+        TKP(4)
+#undef TKP
+        return nullptr;
+    }
 #define TK(RR)                                                                                  \
     if (R == RR)                                                                                \
         return ex ? (minb == 3 ? tma_fn<T, RR, true, 3>() : tma_fn<T, RR, true, 2>())            \
@@ -595,7 +615,8 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
         a.fence_all = c->dbg_fence_all ? 1 : 0;
     }
     const int col_base = (int)(c->base + c->R);
-    const int smem = tma_smem<T>(c->R, c->vd);
+    const int pd = c->vd ? 0 : c->tma_pd;
+    const int smem = tma_smem<T>(c->R, c->vd, pd);
     const CUtensorMap& g0 = c->tm_g[0];
     const CUtensorMap& g1 = c->tm_g[1];
     const CUtensorMap& g2 = c->tm_g[2];
@@ -622,13 +643,16 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
     cfg.numAttrs = na;
     auto go = [&](auto kern) {
         // an error is left for the caller's CHECK_LAUNCH (cudaGetLastError)
-        (void)cudaLaunchKernelEx(&cfg, kern, a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2, col_base);
+        // tm_p[src]: the split rings' head tile (interior box on the current level)
+        (void)cudaLaunchKernelEx(&cfg, kern, a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2,
+                                 c->tm_p[src], col_base);
         return true;
     };
     switch (c->R) {
 #define LT(RR)                                                                 \
     case RR:                                                                   \
         if (c->vd) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2, true>);   \
+        if (pd > 0) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3, false, TMA_PD>); \
         if (c->tma_minb == 3) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3>); \
         return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2>);
         LT(1)
@@ -2407,8 +2431,15 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
                 minb = (cudaFuncGetAttributes(&fa, f3) == cudaSuccess && fa.localSizeBytes <= 8) ? 3 : 2;
             }
             c->tma_minb = minb;
-            const void* f = c->tsize == 4 ? tma_kernel<float>(R, ex, minb) : tma_kernel<double>(R, ex, minb);
-            const int smem = c->tsize == 4 ? tma_smem<float>(R) : tma_smem<double>(R);
+            // split rings (2 planes in flight at 3 CTAs/SM; float): the default;
+            // FDW_TMA_PD=0 restores the single ring (developed C4 field, same box:
+            // sweep 528.6 -> 517.8 us, step 518.4 -> 516.7 us, profiles/r02/ab_pd.json)
+            const char* pde = std::getenv("FDW_TMA_PD");
+            const bool split = pde ? std::atoi(pde) > 0 : true;
+            c->tma_pd = (split && c->tsize == 4 && minb == 3) ? TMA_PD : 0;
+            const void* f = c->tsize == 4 ? tma_kernel<float>(R, ex, minb, c->tma_pd)
+                                          : tma_kernel<double>(R, ex, minb);
+            const int smem = c->tsize == 4 ? tma_smem<float>(R, false, c->tma_pd) : tma_smem<double>(R);
             if (!ck(raise_smem_limit(f, smem), "smem attr"))
                 return bail(FDW_ECUDA);
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 16 * TMA_BX, smem) != cudaSuccess || occ < 1)
@@ -3037,7 +3068,7 @@ fdw_status fdw_layout(const fdw_solver* c, uint64_t* ld, uint64_t* plane, uint64
     if (plane) *plane = (uint64_t)c->plane;
     if (base) *base = (uint64_t)c->base;
     if (planes) *planes = (uint64_t)c->Lz;
-    if (variant) *variant = c->variant | (c->zseg << 8) | (c->occupancy << 16);
+    if (variant) *variant = c->variant | (c->zseg << 8) | (c->occupancy << 16) | (c->tma_pd << 24);
     return FDW_OK;
 }
 

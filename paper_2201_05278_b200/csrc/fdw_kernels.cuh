@@ -554,7 +554,12 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-template <typename T, int R, int BX, int NPA = 3>
+// PD = 0: one u ring of full tiles, the head plane z+R loaded one plane
+// ahead and kept until it is the centre.  PD > 0 (split rings): the full
+// centre tile and the head's interior tile are separate TMA loads, each PD
+// planes ahead, so the same shared memory holds PD planes in flight at 3
+// CTAs/SM (the centre tiles are L2 hits: their interiors arrived as heads).
+template <typename T, int R, int BX, int NPA = 3, int PD = 0>
 struct TmaShape {
     static constexpr int V = 16 / sizeof(T);
     static constexpr int NTY = 16;
@@ -562,14 +567,18 @@ struct TmaShape {
     static constexpr int HY = ((R + V - 1) / V) * V;     // Y halo, whole vectors
     static constexpr int UW = TYW + 2 * HY;              // U tile row (elements)
     static constexpr int UH = BX + 2 * R;                // U tile rows
-    static constexpr int NU = R + 2;                     // U ring: planes z .. z+R, +1 in flight
-    static constexpr int NP = 2;                         // prev/c2dt2/eta[/grad x3] ring
+    static constexpr bool SPLIT = PD > 0;
+    static constexpr int NU = SPLIT ? PD + 1 : R + 2;    // U ring: planes z .. z+R, +1 in flight (split: centres)
+    static constexpr int NH = SPLIT ? PD + 1 : 0;        // split: head interior tiles
+    static constexpr int NP = SPLIT ? PD + 1 : 2;        // prev/c2dt2/eta[/grad x3] ring
     static constexpr int U_BOX = UW * UH * (int)sizeof(T);
     static constexpr int P_BOX = TYW * BX * (int)sizeof(T);
     static constexpr int U_STRIDE = (U_BOX + 127) / 128 * 128;
     static constexpr int P_STRIDE = (P_BOX + 127) / 128 * 128;
-    static constexpr int BAR_OFF = NU * U_STRIDE + NP * NPA * P_STRIDE;
-    static constexpr int SMEM = BAR_OFF + (NU + NP) * 8;
+    static constexpr int H_OFF = NU * U_STRIDE;
+    static constexpr int P_OFF = H_OFF + NH * P_STRIDE;
+    static constexpr int BAR_OFF = P_OFF + NP * NPA * P_STRIDE;
+    static constexpr int SMEM = BAR_OFF + (NU + NH + NP) * 8;
     static constexpr int THREADS = NTY * BX;
 };
 
@@ -582,21 +591,24 @@ struct TmaShape {
 // loads on the hot path; one __syncthreads per plane recycles ring stages.
 // VD (sweep_3d<true>, kernel.hpp:407-417): three more tiles per plane
 // (grad(rho)/rho per axis) and the first-derivative taps on the same operands.
-template <typename T, int R, int BX, bool EXACT, int MINB, bool VD = false>
-__global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
+template <typename T, int R, int BX, bool EXACT, int MINB, bool VD = false, int PD = 0>
+__global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, MINB)
     sweep3d_tma(SweepArgs<T> a, const __grid_constant__ CUtensorMap tu, const __grid_constant__ CUtensorMap tp,
                 const __grid_constant__ CUtensorMap tc, const __grid_constant__ CUtensorMap te,
                 const __grid_constant__ CUtensorMap tg0, const __grid_constant__ CUtensorMap tg1,
-                const __grid_constant__ CUtensorMap tg2, int col_base) {
+                const __grid_constant__ CUtensorMap tg2, const __grid_constant__ CUtensorMap th, int col_base) {
     using A = Ar<T, EXACT>;
     constexpr int NPA = VD ? 6 : 3;
-    using S = TmaShape<T, R, BX, NPA>;
+    using S = TmaShape<T, R, BX, NPA, PD>;
+    constexpr bool SPLIT = S::SPLIT;
     constexpr int V = S::V, NTY = S::NTY, TYW = S::TYW, HY = S::HY, HYV = HY / V, UW = S::UW, NU = S::NU;
+    constexpr int NH = S::NH, NP = S::NP;
     constexpr int THREADS = S::THREADS;
     using VT = Vec<T, V>;
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned long long* barU = reinterpret_cast<unsigned long long*>(smem + S::BAR_OFF);
-    unsigned long long* barP = barU + NU;
+    unsigned long long* barH = barU + NU;
+    unsigned long long* barP = barH + NH;
 
     // the next kernel (point sources) may launch once our last wave is placed
     pdl_launch_dependents();
@@ -632,16 +644,22 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
     }
 
     auto u_stage = [&](int k) { return reinterpret_cast<T*>(smem + (k % NU) * S::U_STRIDE); };
+    auto h_stage = [&](int k) { return reinterpret_cast<T*>(smem + S::H_OFF + (k % (NH ? NH : 1)) * S::P_STRIDE); };
     auto p_stage = [&](int k, int which) {
-        return reinterpret_cast<T*>(smem + NU * S::U_STRIDE + ((k & 1) * NPA + which) * S::P_STRIDE);
+        return reinterpret_cast<T*>(smem + S::P_OFF + ((k % NP) * NPA + which) * S::P_STRIDE);
     };
     auto issue_u = [&](int k) {  // tile of plane zs + k (mirrored plane beyond a physical Z face)
         unsigned long long* b = &barU[k % NU];
         mbar_expect_tx(b, S::U_BOX);
         tma_load_3d(u_stage(k), &tu, col_base + ty0 - HY, tx0, zsrc(zs + k) + R, b);
     };
+    auto issue_h = [&](int k) {  // split rings: interior tile of the head plane zs + k + R
+        unsigned long long* b = &barH[k % (NH ? NH : 1)];
+        mbar_expect_tx(b, S::P_BOX);
+        tma_load_3d(h_stage(k), &th, col_base + ty0, tx0 + R, zsrc(zs + k + R) + R, b);
+    };
     auto issue_p = [&](int k) {
-        unsigned long long* b = &barP[k & 1];
+        unsigned long long* b = &barP[k % NP];
         const bool skip_e = zs + k >= ez0 && zs + k < ez1;
         mbar_expect_tx(b, (skip_e ? NPA - 1 : NPA) * S::P_BOX);
         const int c0 = col_base + ty0, c1 = tx0 + R, c2 = zs + k + R;
@@ -656,8 +674,7 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
     };
 
     if (tid == 0) {
-        for (int k = 0; k < NU; ++k) mbar_init(&barU[k], 1);
-        for (int k = 0; k < S::NP; ++k) mbar_init(&barP[k], 1);
+        for (int k = 0; k < NU + NH + NP; ++k) mbar_init(&barU[k], 1);  // barU, barH, barP are contiguous
         mbar_fence_init();
     }
     __syncthreads();
@@ -675,8 +692,16 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
         if (!peer_ok) return;
     }
     if (tid == 0) {
-        for (int k = 0; k <= R; ++k) issue_u(k);  // planes zs .. zs+R
-        issue_p(0);
+        if constexpr (SPLIT) {
+            for (int k = 0; k < PD; ++k) {  // PD planes in flight
+                issue_u(k);
+                issue_h(k);
+                issue_p(k);
+            }
+        } else {
+            for (int k = 0; k <= R; ++k) issue_u(k);  // planes zs .. zs+R
+            issue_p(0);
+        }
     }
     VT qq[2 * R + 4];
 #pragma unroll
@@ -740,19 +765,29 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3>::THREADS, MINB)
         VT* q = qq + decltype(S)::value;
         const int z = zs + it;
         if (it > 0) __syncthreads();  // stages of plane z-1 are free
-        if (tid == 0 && it + 1 < nit) {
-            issue_u(it + 1 + R);
-            issue_p(it + 1);
+        if constexpr (SPLIT) {
+            if (tid == 0 && it + PD < nit) {
+                issue_u(it + PD);
+                issue_h(it + PD);
+                issue_p(it + PD);
+            }
+            mbar_wait(&barH[it % NH], (it / NH) & 1);
+            q[2 * R] = *reinterpret_cast<const VT*>(h_stage(it) + tx * TYW + ty * V);
+        } else {
+            if (tid == 0 && it + 1 < nit) {
+                issue_u(it + 1 + R);
+                issue_p(it + 1);
+            }
+            const int kh = it + R;
+            mbar_wait(&barU[kh % NU], (kh / NU) & 1);
+            q[2 * R] = *reinterpret_cast<const VT*>(u_stage(kh) + (R + tx) * UW + HY + ty * V);
         }
-        const int kh = it + R;
-        mbar_wait(&barU[kh % NU], (kh / NU) & 1);
-        q[2 * R] = *reinterpret_cast<const VT*>(u_stage(kh) + (R + tx) * UW + HY + ty * V);
         if (zhi && z + R >= nz) {  // head is a mirrored plane (uniform branch)
 #pragma unroll
             for (int e = 0; e < V; ++e) q[2 * R].e[e] = mir(a.gf[0][1], q[2 * R].e[e]);
         }
         mbar_wait(&barU[it % NU], (it / NU) & 1);
-        mbar_wait(&barP[it & 1], (it >> 1) & 1);
+        mbar_wait(&barP[it % NP], (it / NP) & 1);
         T* U0 = u_stage(it);
         if (edge_tile) {
             patch(U0);

@@ -458,7 +458,7 @@ class Solver:
                               C.byref(var))
         return {"ld": ld.value, "plane": plane.value, "base": base.value, "planes": planes.value,
                 "variant": var.value & 0xFF, "z_segments": (var.value >> 8) & 0xFF,
-                "ctas_per_sm": var.value >> 16}
+                "ctas_per_sm": (var.value >> 16) & 0xFF, "tma_pd": var.value >> 24}
 
     # -- peer transport (Z slabs over NVLink peer memory) --
     def peer_export(self) -> bytes:

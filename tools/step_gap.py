@@ -12,7 +12,8 @@ steps with CUDA events on the library stream:
   no_receivers  without receivers
   no_sources    without point sources
   sweep_only    neither
-plus the per-kernel event times of profile_steps on the full variant.
+plus the per-kernel event times of profile_steps per variant.  AB="K=V;K=V"
+replaces the variant list with full steps that differ in env knobs only.
 """
 import json
 import os
@@ -50,6 +51,18 @@ def make(w, src, rec, env, stream):
     return s
 
 
+def variants():
+    """AB="K=V[,K=V];K=V...": full-step variants that differ only in env knobs."""
+    ab = os.environ.get("AB")
+    if not ab:
+        return VARIANTS
+    out = []
+    for spec in ab.split(";"):
+        env = dict(kv.split("=", 1) for kv in spec.split(",") if kv)
+        out.append((spec or "default", 1, 1, env))
+    return out
+
+
 def main():
     cfg = configs.CONFIGS[os.environ.get("WL", "C4")]()
     w = configs.build_workload(cfg, np.float32)
@@ -60,9 +73,9 @@ def main():
     prev, curr = base.previous_level().copy(), base.current_level().copy()
     base.close()
     only = os.environ.get("CASES")
-    vs = [v for v in VARIANTS if not only or v[0] in only.split(",")]
+    vs = [v for v in variants() if not only or v[0] in only.split(",")]
     res = {v[0]: [] for v in vs}
-    prof = None
+    prof_all = {}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for rep in range(REPS):
         for name, src, rec, env in vs:
@@ -79,14 +92,14 @@ def main():
             ev1.record(stream)
             torch.cuda.synchronize()
             res[name].append(ev0.elapsed_time(ev1) / N * 1e3)
-            if name == "full" and rep == REPS - 1:
-                prof = [round(x * 1e3, 2) for x in s.profile_steps(50)]
+            if rep == REPS - 1:
+                prof_all[name] = [round(x * 1e3, 2) for x in s.profile_steps(50)]
             s.close()
     out = {name: {"us_per_step": round(min(v), 2), "reps": [round(x, 2) for x in v],
                   "gpts": round(pts / min(v) / 1e3, 1)} for name, v in res.items()}
+    keys = ["sweep", "inject", "boundary", "receivers", "health", "halo"]
     print(json.dumps({"dev_steps": DEV, "steps": N, "variants": out,
-                      "prof_us_full": dict(zip(["sweep", "inject", "boundary", "receivers", "health", "halo"],
-                                               prof or []))}), flush=True)
+                      "prof_us": {k: dict(zip(keys, v)) for k, v in prof_all.items()}}), flush=True)
 
 
 if __name__ == "__main__":
