@@ -1994,7 +1994,7 @@ const char* fdw_last_error(const fdw_solver* c) { return c ? c->err.c_str() : g_
 
 fdw_status fdw_slab_range(uint64_t n_ext, int32_t world, int32_t rank, uint64_t* zb, uint64_t* ze) {
     if (world < 1 || rank < 0 || rank >= world || n_ext < (uint64_t)world) return FDW_EINVAL;
-    // balanced split, larger slabs first (217 over 8 -> 28 x1, 27 x7)
+    // balanced split, floor(n*r/w) boundaries (217 over 8 -> 27 x7, then 28)
     *zb = n_ext * (uint64_t)rank / (uint64_t)world;
     *ze = n_ext * (uint64_t)(rank + 1) / (uint64_t)world;
     return FDW_OK;

@@ -122,6 +122,27 @@ def test_run_on_slabs_identical_to_the_cpu_reference(tmp_path, devices, dtype, s
             assert open(os.path.join(a, f), "rb").read() == open(os.path.join(b, f), "rb").read(), f
 
 
+@pytest.mark.parametrize("ndim", [2, 3])
+def test_run_verbose_progress_matches_the_cpu_reference(tmp_path, ndim):
+    """`run --verbose` (runner.hpp:84 set_verbose): the reference prints
+    "step s/N  t s  max|p| = m" at every health check (kernel.hpp:459-466).
+    The drop-in must print the same lines -- same steps, same max|p| digits --
+    with only the elapsed time differing."""
+    import re
+    cfg = _config(str(tmp_path), ndim, "float32", 0, False)
+    pat = re.compile(r"^step (\d+)/(\d+)  (\d+\.\d{3})s  max\|p\| = (\S+)$")
+    got = {}
+    for name in ("fdwave_cpu", "fdwave_cuda"):
+        r = subprocess.run([_exe(name), "run", "--config", cfg, "--out", str(tmp_path / name), "--verbose"],
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr
+        lines = [m.groups() for m in (pat.match(l) for l in r.stderr.splitlines()) if m]
+        assert lines, r.stderr
+        got[name] = [(a, b, d) for a, b, _, d in lines]
+    assert got["fdwave_cuda"] == got["fdwave_cpu"]
+    assert got["fdwave_cpu"][-1][0] == got["fdwave_cpu"][-1][1]  # the last step is checked
+
+
 def test_run_instability_exit_code(tmp_path):
     cfg = _config(str(tmp_path), 2, "float32", 0, False, dt=5e-3)  # far above the CFL bound
     for name in ("fdwave_cpu", "fdwave_cuda"):

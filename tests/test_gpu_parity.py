@@ -146,3 +146,28 @@ def test_two_solvers_interleaved():
         o.set_receivers(w.receivers)
         ref = o.forward()
         assert same(r.seismogram.data, ref["seismogram"])
+
+
+def test_verbose_progress_line(capsys):
+    """Solver.set_verbose(True): the reference's line at every health check
+    (kernel.hpp:456-466), "step s/N  t s  max|p| = m", with max|p| the
+    oracle's max_abs at that step."""
+    import re
+    w = build_workload(small_config(ndim=3, order=4, shape=(19, 23, 21), steps=230), np.float32)
+    g = gpu_solver(w)
+    g.set_sources(w.sources, w.wavelet)
+    g.set_verbose(True)
+    g.forward()
+    err = capsys.readouterr().err
+    pat = re.compile(r"^step (\d+)/(\d+)  \d+\.\d{3}s  max\|p\| = (\S+)$")
+    lines = [m.groups() for m in (pat.match(l) for l in err.splitlines()) if m]
+    assert [int(a) for a, _, _ in lines] == [100, 200, 230] and all(b == "230" for _, b, _ in lines)
+    o = oracle_solver(w)
+    o.set_sources(w.sources, w.wavelet)
+    o.refresh_boundary()
+    want = []
+    for k in range(1, 231):
+        o.step()
+        if k % 100 == 0 or k == 230:
+            want.append("%.6e" % o.max_abs())
+    assert [m for _, _, m in lines] == want
