@@ -150,6 +150,11 @@ struct fdw_solver {
     int occupancy = 0;
     int tma_minb = 3;
     int tma_pd = 0;  // > 0: split-ring TMA sweep with that many planes in flight
+    // damping table (split-ring fp32 sweep): 1-byte eta index per point, (om, iop) per index
+    unsigned char* d_eidx = nullptr;
+    float2* d_etab = nullptr;
+    int n_etab = 0;          // entries incl. index 0; 0: no table (the sweep streams fp32 eta)
+    CUtensorMap tm_eb{};     // TMA map over d_eidx
 
     std::map<std::tuple<unsigned long long, int, int, int>, cudaGraphExec_t> graphs;
     std::map<std::tuple<unsigned long long, int, int, int>, unsigned long long> graph_kernels;
@@ -445,6 +450,8 @@ SweepArgs<T> sweep_args(fdw_solver* c, int src, int dst) {
     a.ctrl = c->ctrl;
     a.ezr = c->d_ezr;
     a.seg_rot = 0;
+    a.etab = c->d_etab;
+    a.n_etab = c->n_etab;
     a.negz = static_cast<T>(-0.0);
     if (c->vd) {
         a.vd = 1;
@@ -558,7 +565,19 @@ const void* tma_vd_kernel(int R, bool ex) {
 
 // minb: 2 or 3 resident CTAs requested from ptxas (register cap 128 / 80)
 template <typename T>
-const void* tma_kernel(int R, bool ex, int minb, int pd = 0) {
+const void* tma_kernel(int R, bool ex, int minb, int pd = 0, bool etab = false) {
+    if constexpr (std::is_same<T, float>::value) {
+        if (pd > 0 && etab) {  // split rings with the damping table
+#define TKE(RR) \
+    if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 3, false, TMA_PD, true> \
+                           : (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, false, 3, false, TMA_PD, true>;
+            TKE(1)
+            TKE(2)
+            TKE(4)
+#undef TKE
+            return nullptr;
+        }
+    }
     if (pd > 0) {  // split rings: 3 CTAs/SM only
 #define TKP(RR) \
     if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 3, false, TMA_PD> \
@@ -616,6 +635,7 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
     }
     const int col_base = (int)(c->base + c->R);
     const int pd = c->vd ? 0 : c->tma_pd;
+    const bool etab = pd > 0 && c->n_etab > 0;
     const int smem = tma_smem<T>(c->R, c->vd, pd);
     const CUtensorMap& g0 = c->tm_g[0];
     const CUtensorMap& g1 = c->tm_g[1];
@@ -643,15 +663,22 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
     cfg.numAttrs = na;
     auto go = [&](auto kern) {
         // an error is left for the caller's CHECK_LAUNCH (cudaGetLastError)
-        // tm_p[src]: the split rings' head tile (interior box on the current level)
-        (void)cudaLaunchKernelEx(&cfg, kern, a, c->tm_u[src], c->tm_p[dst], c->tm_c, c->tm_e, g0, g1, g2,
-                                 c->tm_p[src], col_base);
+        // tm_p[src]: the split rings' head tile (interior box on the current level);
+        // with the damping table the eta stream is the 1-byte index map
+        (void)cudaLaunchKernelEx(&cfg, kern, a, c->tm_u[src], c->tm_p[dst], c->tm_c, etab ? c->tm_eb : c->tm_e, g0,
+                                 g1, g2, c->tm_p[src], col_base);
         return true;
     };
+
     switch (c->R) {
 #define LT(RR)                                                                 \
     case RR:                                                                   \
         if (c->vd) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2, true>);   \
+        if (pd > 0 && etab) {                                                  \
+            if constexpr (std::is_same<T, float>::value)                       \
+                return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3, false, TMA_PD, true>); \
+            return false;                                                      \
+        }                                                                      \
         if (pd > 0) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3, false, TMA_PD>); \
         if (c->tma_minb == 3) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3>); \
         return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2>);
@@ -980,14 +1007,18 @@ CUtensorMapL2promotion promo_env(const char* name, int dflt) {
 
 // 3D map over one pitched level: dims (ld, rows_alloc, planes), box (bw, bh, 1)
 bool make_map(const fdw_solver* c, CUtensorMap* m, void* base, int bw, int bh,
-              CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
+              CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B, int esize = 0) {
     auto fn = encode_fn();
     if (!fn) return false;
+    if (!esize) esize = c->tsize;
     const cuuint64_t dims[3] = {(cuuint64_t)c->ld, (cuuint64_t)c->rows_alloc, (cuuint64_t)(c->Lz + 1)};
-    const cuuint64_t strides[2] = {(cuuint64_t)c->ld * c->tsize, (cuuint64_t)c->plane * c->tsize};
+    const cuuint64_t strides[2] = {(cuuint64_t)c->ld * esize, (cuuint64_t)c->plane * esize};
     const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = fn(m, c->tsize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+    const CUtensorMapDataType dt = esize == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                   : esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+    const CUresult r = fn(m, dt, 3,
                           base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                           CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -2499,6 +2530,8 @@ fdw_status fdw_destroy(fdw_solver* c) {
     for (void* p : {(void*)c->d_blk_toff, (void*)c->d_blk_tgt, (void*)c->d_blk_tpos, (void*)c->d_blk_roff,
                     (void*)c->d_blk_rpack, (void*)c->d_tap_ix, c->d_tapbuf})
         if (p) cudaFreeAsync(p, c->stream);
+    for (void* p : {(void*)c->d_eidx, (void*)c->d_etab})
+        if (p) cudaFreeAsync(p, c->stream);
     for (void* p : {(void*)c->d_ezr, (void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off, (void*)c->d_ent_w, (void*)c->d_wavelet,
                     (void*)c->d_rec_idx, (void*)c->d_rec_off, (void*)c->d_rec_w, (void*)c->d_seis, (void*)c->d_tmap})
         if (p) cudaFreeAsync(p, c->stream);
@@ -2524,6 +2557,70 @@ fdw_status fdw_set_stream(fdw_solver* c, void* stream) {
         CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
     }
+    return FDW_OK;
+}
+
+// The damping table of the split-ring fp32 sweep (fdw_kernels.cuh eta_collect):
+// distinct non-zero eta values on the device, indexed on the host in value
+// order, (1 - eta dt, 1/(1 + eta dt)) formed in double exactly as
+// kernel.hpp:284-287, then a 1-byte index per point.  More than 255 distinct
+// values: no table (the sweep streams fp32 eta as before).
+static fdw_status build_eta_table(fdw_solver* c) {
+    c->n_etab = 0;
+    if (std::getenv("FDW_NO_ETAB") || c->tsize != 4 || c->variant != FDW_KERNEL_TMA || c->tma_pd == 0) return FDW_OK;
+    const unsigned long long n = c->level_elems;
+    unsigned* keys = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&keys), (fdw::ETAB_CAP + 1) * sizeof(unsigned), c->stream));
+    CU(cudaMemsetAsync(keys, 0xFF, fdw::ETAB_CAP * sizeof(unsigned), c->stream));
+    CU(cudaMemsetAsync(keys + fdw::ETAB_CAP, 0, sizeof(unsigned), c->stream));
+    fdw::eta_collect<<<c->sm_count * 8, 256, 0, c->stream>>>(static_cast<const float*>(c->eta), n, keys,
+                                                              keys + fdw::ETAB_CAP);
+    CHECK_LAUNCH();
+    std::vector<unsigned> h(fdw::ETAB_CAP + 1);
+    CU(cudaMemcpyAsync(h.data(), keys, h.size() * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    std::vector<float> vals;
+    for (int k = 0; k < fdw::ETAB_CAP; ++k)
+        if (h[k] != fdw::ETAB_EMPTY) {
+            float f;
+            std::memcpy(&f, &h[k], 4);
+            vals.push_back(f);
+        }
+    if (h[fdw::ETAB_CAP] || vals.size() > 255) {
+        cudaFreeAsync(keys, c->stream);
+        return FDW_OK;
+    }
+    std::sort(vals.begin(), vals.end());
+    std::vector<float2> tab(256, make_float2(1.0f, 1.0f));
+    std::vector<unsigned char> slot(fdw::ETAB_CAP, 0);
+    for (size_t i = 0; i < vals.size(); ++i) {
+        volatile double edt = static_cast<double>(vals[i]) * c->d.dt;  // no contraction: as damping_factors
+        const double e = edt;
+        tab[i + 1] = make_float2(static_cast<float>(1.0 - e), static_cast<float>(1.0 / (1.0 + e)));
+        unsigned bits;
+        std::memcpy(&bits, &vals[i], 4);
+        for (int k = 0; k < fdw::ETAB_CAP; ++k)
+            if (h[k] == bits) slot[k] = static_cast<unsigned char>(i + 1);
+    }
+    unsigned char* d_slot = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&d_slot), fdw::ETAB_CAP, c->stream));
+    CU(cudaMemcpyAsync(d_slot, slot.data(), fdw::ETAB_CAP, cudaMemcpyHostToDevice, c->stream));
+    if (!c->d_etab) CU(cudaMallocAsync(reinterpret_cast<void**>(&c->d_etab), 256 * sizeof(float2), c->stream));
+    CU(cudaMemcpyAsync(c->d_etab, tab.data(), 256 * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
+    if (!c->d_eidx) CU(cudaMallocAsync(reinterpret_cast<void**>(&c->d_eidx), n, c->stream));
+    fdw::eta_index<<<c->sm_count * 8, 256, 0, c->stream>>>(static_cast<const float*>(c->eta), n, keys, d_slot,
+                                                            c->d_eidx);
+    CHECK_LAUNCH();
+    cudaFreeAsync(keys, c->stream);
+    cudaFreeAsync(d_slot, c->stream);
+    if (!make_map(c, &c->tm_eb, c->d_eidx, fdw::TmaShape<float, 1, TMA_BX>::TYW, TMA_BX,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, 1))
+        return fail(c, FDW_ECUDA, "cuTensorMapEncodeTiled failed (eta index map)");
+    const bool ex = c->d.math == FDW_MATH_EXACT;
+    const void* f = tma_kernel<float>(c->R, ex, 3, c->tma_pd, true);
+    if (!f) return FDW_OK;
+    CU(raise_smem_limit(f, tma_smem<float>(c->R, false, c->tma_pd)));
+    c->n_etab = (int)vals.size() + 1;
     return FDW_OK;
 }
 
@@ -2559,6 +2656,9 @@ fdw_status fdw_set_medium(fdw_solver* c, const void* velocity, const void* eta, 
                 (int)c->nyl, TMA_BX, tyw, c->d_ezr);
         CHECK_LAUNCH();
     }
+    if ((s = build_eta_table(c))) return s;
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);  // a table may have appeared or gone
+    c->graphs.clear();
     CU(cudaStreamSynchronize(c->stream));
     pt.lap("sync");
     c->medium_set = true;

@@ -255,6 +255,10 @@ struct SweepArgs {
     // TMA sweep: per tile column, the Z range [x, y) of planes whose eta tile
     // is all zero (those planes skip the eta stream); null: none
     const int2* ezr;
+    // split-ring fp32 sweep with a damping table: (1 - eta dt, 1/(1 + eta dt))
+    // per index, index 0 = undamped; the eta map then streams 1-byte indices
+    const float2* etab;
+    int n_etab;
     // TMA sweep Z segments: CTA z-index b sweeps segment (b + seg_rot) mod
     // gridDim.z; a slab rotates its boundary segments (S-1, 0) into the first
     // wave so the halo stores and the epoch publish happen early in the step.
@@ -591,7 +595,7 @@ struct TmaShape {
 // loads on the hot path; one __syncthreads per plane recycles ring stages.
 // VD (sweep_3d<true>, kernel.hpp:407-417): three more tiles per plane
 // (grad(rho)/rho per axis) and the first-derivative taps on the same operands.
-template <typename T, int R, int BX, bool EXACT, int MINB, bool VD = false, int PD = 0>
+template <typename T, int R, int BX, bool EXACT, int MINB, bool VD = false, int PD = 0, bool ETAB = false>
 __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, MINB)
     sweep3d_tma(SweepArgs<T> a, const __grid_constant__ CUtensorMap tu, const __grid_constant__ CUtensorMap tp,
                 const __grid_constant__ CUtensorMap tc, const __grid_constant__ CUtensorMap te,
@@ -604,6 +608,8 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
     constexpr int V = S::V, NTY = S::NTY, TYW = S::TYW, HY = S::HY, HYV = HY / V, UW = S::UW, NU = S::NU;
     constexpr int NH = S::NH, NP = S::NP;
     constexpr int THREADS = S::THREADS;
+    static_assert(!ETAB || (std::is_same<T, float>::value && !VD && V == 4), "damping table: fp32 packed path");
+    constexpr int E_BOX = ETAB ? TYW * BX : S::P_BOX;  // bytes of the eta (or eta index) tile
     using VT = Vec<T, V>;
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned long long* barU = reinterpret_cast<unsigned long long*>(smem + S::BAR_OFF);
@@ -661,7 +667,7 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
     auto issue_p = [&](int k) {
         unsigned long long* b = &barP[k % NP];
         const bool skip_e = zs + k >= ez0 && zs + k < ez1;
-        mbar_expect_tx(b, (skip_e ? NPA - 1 : NPA) * S::P_BOX);
+        mbar_expect_tx(b, (NPA - 1) * S::P_BOX + (skip_e ? 0 : E_BOX));
         const int c0 = col_base + ty0, c1 = tx0 + R, c2 = zs + k + R;
         tma_load_3d(p_stage(k, 0), &tp, c0, c1, c2, b);
         tma_load_3d(p_stage(k, 1), &tc, c0, c1, c2, b);
@@ -677,6 +683,9 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
         for (int k = 0; k < NU + NH + NP; ++k) mbar_init(&barU[k], 1);  // barU, barH, barP are contiguous
         mbar_fence_init();
     }
+    __shared__ float2 s_etab[ETAB ? 256 : 1];
+    if constexpr (ETAB)
+        for (int k = tid; k < a.n_etab; k += THREADS) s_etab[k] = a.etab[k];
     __syncthreads();
     // everything above touches shared memory and setup-time data only
     pdl_wait();
@@ -854,6 +863,22 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
                     const float2 r2 = sub2(mac2(mul2(two, pr(q[R], p), nz2), pr(cc, p), rhs2[p]), pr(pc, p));
                     res.e[2 * p] = r2.x;
                     res.e[2 * p + 1] = r2.y;
+                }
+            } else if constexpr (ETAB) {
+                // time_update with the tabled factors (index 0: eta == 0, undamped)
+                const uchar4 ib = *reinterpret_cast<const uchar4*>(
+                    reinterpret_cast<const unsigned char*>(p_stage(it, 2)) + po);
+                const unsigned ix[4] = {ib.x, ib.y, ib.z, ib.w};
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    const T rhs = (e & 1) ? rhs2[e >> 1].y : rhs2[e >> 1].x;
+                    const T t = A::add(A::mul(cc.e[e], rhs), A::mul(T(2), q[R].e[e]));
+                    if (ix[e] == 0) {
+                        res.e[e] = A::sub(t, pc.e[e]);
+                    } else {
+                        const float2 f = s_etab[ix[e]];
+                        res.e[e] = A::mul(A::sub(t, A::mul(f.x, pc.e[e])), f.y);
+                    }
                 }
             } else {
                 const VT ec = *reinterpret_cast<const VT*>(p_stage(it, 2) + po);
@@ -2566,6 +2591,60 @@ __global__ void eta_zero_ranges(const T* __restrict__ eta, long long origin, lon
             run0 = z + 1;
         }
         out[col] = make_int2(best0, best1);
+    }
+}
+
+// Damping table (fp32 TMA sweep): when the damping field takes at most 255
+// distinct non-zero values -- damping_field (model.hpp:141-186) gives a few
+// dozen: eta depends only on the distance to the physical box -- the sweep
+// streams a 1-byte index per point instead of the 4-byte eta, and reads
+// (1 - eta dt, 1 / (1 + eta dt)) from a table formed on the host in double
+// exactly as kernel.hpp:284-287 (bit-identical to forming them per point).
+// Pass 1: distinct non-zero bit patterns into an open-addressing set.
+constexpr int ETAB_CAP = 1024;  // set slots (power of two)
+constexpr unsigned ETAB_EMPTY = 0xFFFFFFFFu;
+__device__ __forceinline__ unsigned etab_hash(unsigned v) {
+    v ^= v >> 16;
+    v *= 0x7feb352du;
+    v ^= v >> 15;
+    return v & (ETAB_CAP - 1);
+}
+__global__ void eta_collect(const float* __restrict__ eta, unsigned long long n, unsigned* keys, unsigned* overflow) {
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const float f = eta[i];
+        if (f == 0.0f) continue;
+        const unsigned v = __float_as_uint(f);
+        unsigned h = etab_hash(v);
+        for (int probe = 0;; ++probe) {
+            const unsigned k = *reinterpret_cast<volatile unsigned*>(&keys[h]);
+            if (k == v) break;
+            if (k == ETAB_EMPTY) {
+                const unsigned old = atomicCAS(&keys[h], ETAB_EMPTY, v);
+                if (old == ETAB_EMPTY || old == v) break;
+            }
+            if (probe >= ETAB_CAP) {
+                atomicOr(overflow, 1u);
+                break;
+            }
+            h = (h + 1) & (ETAB_CAP - 1);
+        }
+    }
+}
+// Pass 2: the index of every point (0: eta == 0, undamped).
+__global__ void eta_index(const float* __restrict__ eta, unsigned long long n, const unsigned* __restrict__ keys,
+                          const unsigned char* __restrict__ slot_index, unsigned char* __restrict__ out) {
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const float f = eta[i];
+        unsigned char ix = 0;
+        if (f != 0.0f) {
+            const unsigned v = __float_as_uint(f);
+            unsigned h = etab_hash(v);
+            while (keys[h] != v) h = (h + 1) & (ETAB_CAP - 1);
+            ix = slot_index[h];
+        }
+        out[i] = ix;
     }
 }
 
