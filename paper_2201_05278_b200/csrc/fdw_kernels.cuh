@@ -865,20 +865,21 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
                     res.e[2 * p + 1] = r2.y;
                 }
             } else if constexpr (ETAB) {
-                // time_update with the tabled factors (index 0: eta == 0, undamped)
+                // time_update with the tabled factors, two lanes per instruction.
+                // Index 0 (eta == 0) holds (1, 1): x * 1 == x exactly (signed
+                // zeros, subnormals, NaN), so the damped form reproduces the
+                // undamped (t - prev) bit for bit and no lane branches.
                 const uchar4 ib = *reinterpret_cast<const uchar4*>(
                     reinterpret_cast<const unsigned char*>(p_stage(it, 2)) + po);
-                const unsigned ix[4] = {ib.x, ib.y, ib.z, ib.w};
+                const float2 f0 = s_etab[ib.x], f1 = s_etab[ib.y], f2 = s_etab[ib.z], f3 = s_etab[ib.w];
+                const float2 om[2] = {make_float2(f0.x, f1.x), make_float2(f2.x, f3.x)};
+                const float2 io[2] = {make_float2(f0.y, f1.y), make_float2(f2.y, f3.y)};
 #pragma unroll
-                for (int e = 0; e < V; ++e) {
-                    const T rhs = (e & 1) ? rhs2[e >> 1].y : rhs2[e >> 1].x;
-                    const T t = A::add(A::mul(cc.e[e], rhs), A::mul(T(2), q[R].e[e]));
-                    if (ix[e] == 0) {
-                        res.e[e] = A::sub(t, pc.e[e]);
-                    } else {
-                        const float2 f = s_etab[ix[e]];
-                        res.e[e] = A::mul(A::sub(t, A::mul(f.x, pc.e[e])), f.y);
-                    }
+                for (int p = 0; p < 2; ++p) {
+                    const float2 t2 = mac2(mul2(two, pr(q[R], p), nz2), pr(cc, p), rhs2[p]);
+                    const float2 r2 = mul2(sub2(t2, mul2(om[p], pr(pc, p), nz2)), io[p], nz2);
+                    res.e[2 * p] = r2.x;
+                    res.e[2 * p + 1] = r2.y;
                 }
             } else {
                 const VT ec = *reinterpret_cast<const VT*>(p_stage(it, 2) + po);
