@@ -1011,7 +1011,14 @@ bool make_map(const fdw_solver* c, CUtensorMap* m, void* base, int bw, int bh,
     auto fn = encode_fn();
     if (!fn) return false;
     if (!esize) esize = c->tsize;
-    const cuuint64_t dims[3] = {(cuuint64_t)c->ld, (cuuint64_t)c->rows_alloc, (cuuint64_t)(c->Lz + 1)};
+    // The tensor ends at the padded box: row / column slack beyond it is
+    // out of bounds, which TMA zero-fills without touching DRAM (the last
+    // tile of a row or column would otherwise stream up to 63 slack columns /
+    // 15 slack rows of every field).  No kernel reads a value from there.
+    // FDW_TMA_FULL_PITCH=1: the whole allocated pitch (A/B).
+    static const bool full = std::getenv("FDW_TMA_FULL_PITCH") != nullptr;
+    const cuuint64_t dims[3] = {(cuuint64_t)(full ? c->ld : c->base + c->P[2]),
+                                (cuuint64_t)(full ? c->rows_alloc : c->P[1]), (cuuint64_t)(c->Lz + 1)};
     const cuuint64_t strides[2] = {(cuuint64_t)c->ld * esize, (cuuint64_t)c->plane * esize};
     const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
