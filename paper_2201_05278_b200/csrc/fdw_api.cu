@@ -529,6 +529,13 @@ constexpr int TMA_PD = 2;  // split-ring prefetch depth (FDW_TMA_PD=2)
 
 template <typename T>
 int tma_smem(int R, bool vd = false, int pd = 0) {
+    if (pd > 0 && vd) {
+        switch (R) {
+            case 1: return fdw::TmaShape<T, 1, TMA_BX, 6, TMA_PD>::SMEM;
+            case 2: return fdw::TmaShape<T, 2, TMA_BX, 6, TMA_PD>::SMEM;
+            default: return fdw::TmaShape<T, 4, TMA_BX, 6, TMA_PD>::SMEM;
+        }
+    }
     if (pd > 0 && !vd) {
         switch (R) {
             case 1: return fdw::TmaShape<T, 1, TMA_BX, 3, TMA_PD>::SMEM;
@@ -552,7 +559,19 @@ int tma_smem(int R, bool vd = false, int pd = 0) {
 
 // variable-density TMA sweep (2 CTAs/SM: 6 tiles per plane stage)
 template <typename T>
-const void* tma_vd_kernel(int R, bool ex) {
+const void* tma_vd_kernel(int R, bool ex, bool fast = false) {
+    if constexpr (std::is_same<T, float>::value) {
+        if (fast) {  // split rings + damping table
+#define TKVF(RR) \
+    if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 2, true, TMA_PD, true> \
+                           : (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, false, 2, true, TMA_PD, true>;
+            TKVF(1)
+            TKVF(2)
+            TKVF(4)
+#undef TKVF
+            return nullptr;
+        }
+    }
 #define TKV(RR) \
     if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 2, true> \
                            : (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, false, 2, true>;
@@ -634,8 +653,9 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
         a.fence_all = c->dbg_fence_all ? 1 : 0;
     }
     const int col_base = (int)(c->base + c->R);
-    const int pd = c->vd ? 0 : c->tma_pd;
-    const bool etab = pd > 0 && c->n_etab > 0;
+    const bool etab = c->tma_pd > 0 && c->n_etab > 0;
+    // density: split rings only together with the damping table (vd_fast)
+    const int pd = c->vd ? (etab ? c->tma_pd : 0) : c->tma_pd;
     const int smem = tma_smem<T>(c->R, c->vd, pd);
     const CUtensorMap& g0 = c->tm_g[0];
     const CUtensorMap& g1 = c->tm_g[1];
@@ -673,6 +693,11 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
     switch (c->R) {
 #define LT(RR)                                                                 \
     case RR:                                                                   \
+        if (c->vd && etab) {                                                   \
+            if constexpr (std::is_same<T, float>::value)                       \
+                return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2, true, TMA_PD, true>); \
+            return false;                                                      \
+        }                                                                      \
         if (c->vd) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2, true>);   \
         if (pd > 0 && etab) {                                                  \
             if constexpr (std::is_same<T, float>::value)                       \
@@ -2700,9 +2725,12 @@ fdw_status fdw_set_density(fdw_solver* c, const void* rho, int on_device) {
             if (!make_map(c, &c->tm_g[ax], c->grad[ax], pw, TMA_BX))
                 return fail(c, FDW_ECUDA, "cuTensorMapEncodeTiled failed (density maps)");
         const bool ex = c->d.math == FDW_MATH_EXACT;
-        const void* f = c->tsize == 4 ? tma_vd_kernel<float>(c->R, ex) : tma_vd_kernel<double>(c->R, ex);
-        const int smem = c->tsize == 4 ? tma_smem<float>(c->R, true) : tma_smem<double>(c->R, true);
+        const bool fast = c->tsize == 4 && c->tma_pd > 0 && c->n_etab > 0;  // as launch_tma chooses
+        const void* f = c->tsize == 4 ? tma_vd_kernel<float>(c->R, ex, fast) : tma_vd_kernel<double>(c->R, ex);
+        const int smem = c->tsize == 4 ? tma_smem<float>(c->R, true, fast ? TMA_PD : 0) : tma_smem<double>(c->R, true);
         CU(raise_smem_limit(f, smem));
+        if (fast)  // a later set_medium may drop the table: keep the single-ring kernel launchable
+            CU(raise_smem_limit(tma_vd_kernel<float>(c->R, ex), tma_smem<float>(c->R, true)));
         int occ = 1;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 16 * TMA_BX, smem) != cudaSuccess || occ < 1)
             occ = 1;

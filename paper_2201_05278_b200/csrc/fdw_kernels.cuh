@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
     constexpr int V = S::V, NTY = S::NTY, TYW = S::TYW, HY = S::HY, HYV = HY / V, UW = S::UW, NU = S::NU;
     constexpr int NH = S::NH, NP = S::NP;
     constexpr int THREADS = S::THREADS;
-    static_assert(!ETAB || (std::is_same<T, float>::value && !VD && V == 4), "damping table: fp32 packed path");
+    static_assert(!ETAB || (std::is_same<T, float>::value && V == 4), "damping table: fp32 only");
     constexpr int E_BOX = ETAB ? TYW * BX : S::P_BOX;  // bytes of the eta (or eta index) tile
     using VT = Vec<T, V>;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -947,6 +947,16 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
     #pragma unroll
                 for (int e = 0; e < V; ++e)
                     res.e[e] = A::sub(A::add(A::mul(cc.e[e], rhs_of(e)), A::mul(T(2), q[R].e[e])), pc.e[e]);
+            } else if constexpr (ETAB) {  // tabled factors; index 0 = (1, 1) is exact
+                const uchar4 ib = *reinterpret_cast<const uchar4*>(
+                    reinterpret_cast<const unsigned char*>(p_stage(it, 2)) + po);
+                const unsigned ix[4] = {ib.x, ib.y, ib.z, ib.w};
+    #pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    const float2 f = s_etab[ix[e]];
+                    const T t = A::add(A::mul(cc.e[e], rhs_of(e)), A::mul(T(2), q[R].e[e]));
+                    res.e[e] = A::mul(A::sub(t, A::mul(f.x, pc.e[e])), f.y);
+                }
             } else {
                 const VT ec = *reinterpret_cast<const VT*>(p_stage(it, 2) + po);
     #pragma unroll
