@@ -1614,16 +1614,26 @@ fdw_status res2d_receivers(fdw_solver* c, const std::vector<long long>& ri) {
         const long long b = res2d_block_of(c, z, x, &pos);
         per[(size_t)b].push_back({e, pos, f});
     }
+    // One tap-buffer slot per distinct (block, position, mirror factor): the
+    // windows of neighbouring receivers overlap (C2: 108,800 entries on 14,7k
+    // points), so the blocks that hold them store each value once per row.
     std::vector<int> off(1, 0), pack, ix((size_t)std::max(n, 1), 0);
     int most = 0;
     for (auto& v : per) {
+        std::unordered_map<int, int> uniq;
         for (auto& t : v) {
-            ix[(size_t)std::get<0>(t)] = (int)pack.size();
-            pack.push_back((std::get<1>(t) << 2) | (std::get<2>(t) + 1));
+            const int key = (std::get<1>(t) << 2) | (std::get<2>(t) + 1);
+            auto it = uniq.find(key);
+            if (it == uniq.end()) {
+                it = uniq.emplace(key, (int)pack.size()).first;
+                pack.push_back(key);
+            }
+            ix[(size_t)std::get<0>(t)] = it->second;
         }
-        most = std::max(most, (int)v.size());
+        most = std::max(most, (int)uniq.size());
         off.push_back((int)pack.size());
     }
+    const int n_slots = (int)pack.size();
     fdw_status s;
     if ((s = dev_upload(c, &c->d_blk_roff, off))) return s;
     if ((s = dev_upload(c, &c->d_blk_rpack, pack))) return s;
@@ -1654,9 +1664,9 @@ fdw_status res2d_receivers(fdw_solver* c, const std::vector<long long>& ri) {
     }
     if (c->d_tapbuf) cudaFreeAsync(c->d_tapbuf, c->stream);
     c->d_tapbuf = nullptr;
-    c->n_ent = n;
-    CU(cudaMallocAsync(&c->d_tapbuf, (size_t)std::max(1, 4 * n) * c->tsize, c->stream));  // 4 rows in flight
-    CU(cudaMemsetAsync(c->d_tapbuf, 0, (size_t)std::max(1, 4 * n) * c->tsize, c->stream));
+    c->n_ent = n_slots;
+    CU(cudaMallocAsync(&c->d_tapbuf, (size_t)std::max(1, 4 * n_slots) * c->tsize, c->stream));  // 4 rows in flight
+    CU(cudaMemsetAsync(c->d_tapbuf, 0, (size_t)std::max(1, 4 * n_slots) * c->tsize, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     return FDW_OK;
 }

@@ -1792,8 +1792,17 @@ __global__ void __launch_bounds__(256) step2d_resident2(Res2DArgs<T> a, int L, i
     // index, 0 = column x0 - H1): out <- in / prev, coefficient arrays at cidx
     auto sweep = [&](const T* In, T* Out, int zA, int zB, int vx0, int vx1, int xlo, int xhi) {
         const int nvr = vx1 - vx0;
+        // (row, vector) of this thread's items, stepped without a division per item
+        const int dz = 256 / nvr, dv = 256 % nvr;
+        int zi = tid / nvr, vi = tid % nvr;
         for (int it = tid; it < (zB - zA) * nvr; it += 256) {
-            const int z = zA + it / nvr, xv = x0 - H1 + (vx0 + it % nvr) * V;
+            const int z = zA + zi, xv = x0 - H1 + (vx0 + vi) * V;
+            zi += dz;
+            vi += dv;
+            if (vi >= nvr) {
+                vi -= nvr;
+                ++zi;
+            }
             if (xv + V <= xlo || xv >= xhi) continue;
             const int o = sidx(z, xv);
             const VT c = *reinterpret_cast<const VT*>(In + o);
@@ -1971,16 +1980,42 @@ __global__ void __launch_bounds__(256) step2d_resident2(Res2DArgs<T> a, int L, i
             }
         }
         grid.sync();
-        // 2R halo of the newest level (corners too): neighbours' strips
+        // 2R halo of the newest level (corners too): neighbours' strips.  Only
+        // the halo is enumerated (2R rows above and below over the slot width,
+        // H2 columns left and right of the block rows), and each thread issues
+        // its L2 loads in batches of four before storing any of them.
         {
             const T* g = a.lvl[cur0];
-            for (int i = tid; i < ROWS * (UW / V); i += 256) {
-                const int r = i / (UW / V), q = i % (UW / V);
-                const int z = z0 - 2 * R + r, x = x0 - H2 + q * V;
-                // own block (incl. its columns past nx), ghost rows / columns: skipped
-                if ((z >= z0 && z < z0 + bz && x >= x0 && x < x0 + TX) || z < 0 || z >= nz || x < 0 || x + V > nx)
-                    continue;
-                *reinterpret_cast<VT*>(sU + sidx(z, x)) = ldcg16(g + gidx(z, x));
+            constexpr int UWV = UW / V, H2V = H2 / V, B = 4;
+            const int n_rows = 2 * R * UWV, n_tot = 2 * n_rows + bz * 2 * H2V;
+            for (int i0 = 0; i0 < n_tot; i0 += B * 256) {
+                VT hv[B];
+                int ho[B];
+#pragma unroll
+                for (int u = 0; u < B; ++u) {
+                    const int i = i0 + u * 256 + tid;
+                    ho[u] = -1;
+                    if (i >= n_tot) continue;
+                    int z, x;
+                    if (i < 2 * n_rows) {  // rows above, then rows below the block
+                        const int j = i < n_rows ? i : i - n_rows;
+                        z = (i < n_rows ? z0 - 2 * R : z0 + bz) + j / UWV;
+                        x = x0 - H2 + (j % UWV) * V;
+                    } else {  // left / right columns of the block rows
+                        const int j = i - 2 * n_rows, q = j % (2 * H2V);
+                        z = z0 + j / (2 * H2V);
+                        x = q < H2V ? x0 - H2 + q * V : x0 + TX + (q - H2V) * V;
+                    }
+                    // own block (incl. its columns past nx), ghost rows / columns: skipped
+                    if ((z >= z0 && z < z0 + bz && x >= x0 && x < x0 + TX) || z < 0 || z >= nz || x < 0 ||
+                        x + V > nx)
+                        continue;
+                    hv[u] = ldcg16(g + gidx(z, x));
+                    ho[u] = sidx(z, x);
+                }
+#pragma unroll
+                for (int u = 0; u < B; ++u)
+                    if (ho[u] >= 0) *reinterpret_cast<VT*>(sU + ho[u]) = hv[u];
             }
         }
         __syncthreads();
