@@ -1665,8 +1665,8 @@ fdw_status res2d_receivers(fdw_solver* c, const std::vector<long long>& ri) {
     if (c->d_tapbuf) cudaFreeAsync(c->d_tapbuf, c->stream);
     c->d_tapbuf = nullptr;
     c->n_ent = n_slots;
-    CU(cudaMallocAsync(&c->d_tapbuf, (size_t)std::max(1, 4 * n_slots) * c->tsize, c->stream));  // 4 rows in flight
-    CU(cudaMemsetAsync(c->d_tapbuf, 0, (size_t)std::max(1, 4 * n_slots) * c->tsize, c->stream));
+    CU(cudaMallocAsync(&c->d_tapbuf, (size_t)std::max(1, 8 * n_slots) * c->tsize, c->stream));  // 8 rows in flight
+    CU(cudaMemsetAsync(c->d_tapbuf, 0, (size_t)std::max(1, 8 * n_slots) * c->tsize, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     return FDW_OK;
 }

@@ -1666,7 +1666,7 @@ struct Res2DShape2 {
 };
 
 template <typename T, int R, bool EXACT>
-__global__ void __launch_bounds__(256) step2d_resident2(Res2DArgs<T> a, int L, int cur0, int record) {
+__global__ void __launch_bounds__(256, 2) step2d_resident2(Res2DArgs<T> a, int L, int cur0, int record) {
     using A = Ar<T, EXACT>;
     using S = Res2DShape2<T, R>;
     constexpr int V = S::V, TX = S::TX, H1 = S::H1, H2 = S::H2, UW = S::UW, CW = S::CW;
@@ -1786,7 +1786,9 @@ __global__ void __launch_bounds__(256) step2d_resident2(Res2DArgs<T> a, int L, i
         __syncwarp();
     };
     auto rec_row = [&](int kk) { return base + (unsigned long long)kk + 1 - row_base; };
-    auto tslot = [&](int kk) { return a.tapbuf + (size_t)(kk & 3) * a.n_ent; };  // 4 rows in flight
+    // 8 rows in flight: a pair's receiver sums run after the grid barrier
+    // (beside the halo loads), so slot kk is free again only two pairs later
+    auto tslot = [&](int kk) { return a.tapbuf + (size_t)(kk & 7) * a.n_ent; };
 
     // one step on the region [zA, zB) x vectors [vx0, vx1) (block-local vector
     // index, 0 = column x0 - H1): out <- in / prev, coefficient arrays at cidx
@@ -1944,7 +1946,9 @@ __global__ void __launch_bounds__(256) step2d_resident2(Res2DArgs<T> a, int L, i
                 }
             }
         }
-        // the previous pair's rows (taps loaded before the sweeps)
+        // the previous pair's rows (taps loaded before the sweeps); run while
+        // the halo loads after the grid barrier are in flight
+        auto recv_prev = [&]() {
         if (rec_prev) {
             if (has_fast && fast_ok && re - rb <= (unsigned)(F2D_CHUNK / 2) && rec_row(k - 1) < a.n_rows) {
                 // both rows at once: products in the two halves of the warp's
@@ -1979,14 +1983,16 @@ __global__ void __launch_bounds__(256) step2d_resident2(Res2DArgs<T> a, int L, i
                 if (rec_row(k - 1) < a.n_rows) rec_slow(rcv, tslot(k - 1), rec_row(k - 1));
             }
         }
+        };
         grid.sync();
         // 2R halo of the newest level (corners too): neighbours' strips.  Only
         // the halo is enumerated (2R rows above and below over the slot width,
-        // H2 columns left and right of the block rows), and each thread issues
-        // its L2 loads in batches of four before storing any of them.
+        // H2 columns left and right of the block rows); each thread issues its
+        // L2 loads in batches before storing any of them, and the first batch
+        // is in flight during the previous pair's receiver sums.
         {
             const T* g = a.lvl[cur0];
-            constexpr int UWV = UW / V, H2V = H2 / V, B = 4;
+            constexpr int UWV = UW / V, H2V = H2 / V, B = 2;
             const int n_rows = 2 * R * UWV, n_tot = 2 * n_rows + bz * 2 * H2V;
             for (int i0 = 0; i0 < n_tot; i0 += B * 256) {
                 VT hv[B];
@@ -2013,10 +2019,12 @@ __global__ void __launch_bounds__(256) step2d_resident2(Res2DArgs<T> a, int L, i
                     hv[u] = ldcg16(g + gidx(z, x));
                     ho[u] = sidx(z, x);
                 }
+                if (i0 == 0) recv_prev();
 #pragma unroll
                 for (int u = 0; u < B; ++u)
                     if (ho[u] >= 0) *reinterpret_cast<VT*>(sU + ho[u]) = hv[u];
             }
+            if (n_tot <= 0) recv_prev();
         }
         __syncthreads();
         // faces of the newest level, over the block + ring (the next step 1 reads them there)
