@@ -1372,12 +1372,14 @@ void peer_leave(fdw_solver* c) {
             if (g->member[r] && g->member[r] != c) cudaStreamSynchronize(g->member[r]->stream);
         g->member[c->d.rank] = nullptr;
         c->group = nullptr;
+        // a broken group is never joined again: drop its key now (a new rank-0
+        // context may reuse this address while other members still live)
+        for (auto it = g_groups.begin(); it != g_groups.end();)
+            it = it->second == g ? g_groups.erase(it) : std::next(it);
         if (--g->alive == 0) {
             for (auto& e2 : g->ev)
                 for (cudaEvent_t e : e2)
                     if (e) cudaEventDestroy(e);
-            for (auto it = g_groups.begin(); it != g_groups.end();)
-                it = it->second == g ? g_groups.erase(it) : std::next(it);
             delete g;
         }
         return;
