@@ -694,13 +694,7 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
     // stores into the neighbour's -> the neighbours must have published this
     // rank's epoch (they finished the previous step)
     const bool plo = a.peer_lo && zs < R, phi = a.peer_hi && ze > nz - R;
-    if (plo || phi) {
-        __shared__ int peer_ok;
-        if (tid == 0) peer_ok = peer_wait_neighbours(a.peer) ? 1 : 0;
-        __syncthreads();
-        if (!peer_ok) return;
-    }
-    if (tid == 0) {
+    auto issue_first = [&]() {
         if constexpr (SPLIT) {
             for (int k = 0; k < PD; ++k) {  // PD planes in flight
                 issue_u(k);
@@ -711,6 +705,34 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
             for (int k = 0; k <= R; ++k) issue_u(k);  // planes zs .. zs+R
             issue_p(0);
         }
+    };
+    if (plo || phi) {
+        // The first TMA loads read owned planes only (unless the segment is
+        // thinner than its head reach): issue them while another warp waits
+        // for the neighbours, so the wait overlaps the load latency.
+        const bool early = !phi || zs + R + (SPLIT ? PD - 1 : 0) < nz;
+        if (tid == 0 && early) issue_first();
+        __shared__ int peer_ok;
+        if (tid == 32) peer_ok = peer_wait_neighbours(a.peer) ? 1 : 0;
+        __syncthreads();
+        if (!peer_ok) {
+            if (tid == 0 && early) {  // no bulk copy may outlive the CTA
+                if constexpr (SPLIT) {
+                    for (int k = 0; k < PD; ++k) {
+                        mbar_wait(&barU[k], 0);
+                        mbar_wait(&barH[k], 0);
+                        mbar_wait(&barP[k], 0);
+                    }
+                } else {
+                    for (int k = 0; k <= R; ++k) mbar_wait(&barU[k], 0);
+                    mbar_wait(&barP[0], 0);
+                }
+            }
+            return;
+        }
+        if (tid == 0 && !early) issue_first();
+    } else if (tid == 0) {
+        issue_first();
     }
     VT qq[2 * R + 4];
 #pragma unroll
