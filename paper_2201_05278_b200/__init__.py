@@ -14,6 +14,7 @@ from .kernel import (Backend, BoundaryCondition, BoundarySpec, FdwError, Forward
                      InstabilityError, ModulatedField, Seismogram, Solver, apply_boundary,
                      boundary_condition_from_string)
 from .model import DampingField, MaterialModel, damping_field, make_material_model, resample_model
+from .multi import SlabSolver
 from .stencil import (StencilCoeffs, first_derivative_coefficients, make_stencil,
                       second_derivative_coefficients, stable_dt)
 from .time_axis import TimeAxis, build_time_axis

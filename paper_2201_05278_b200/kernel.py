@@ -134,9 +134,20 @@ class Solver:
     arrays are the rank's local padded slab; link the ranks with peer_link /
     dist.link_peers before stepping)."""
 
+    def __new__(cls, grid=None, *args, devices=None, slab=None, **kw):
+        """Like the C++ drop-in: several devices (devices=[...], or FDW_DEVICES
+        in the environment) make a 3D Solver a SlabSolver, one Z slab per GPU."""
+        if cls is Solver and slab is None and grid is not None and grid.ndim == 3:
+            from .multi import SlabSolver, devices_from_env
+            devs = list(devices) if devices is not None else devices_from_env()
+            if len(devs) > 1 and grid.extended_shape[0] >= 2 * grid.halo * len(devs):
+                kw.pop("device", None)
+                return SlabSolver(grid, *args, devices=devs, **kw)
+        return super().__new__(cls)
+
     def __init__(self, grid, materials, damping, boundary: BoundarySpec, time_axis, coeffs, *,
                  device: int = 0, variant: int = 0, math: int = 0, z_segments: int = 0,
-                 slab=None):
+                 slab=None, devices=None):
         if coeffs.order != grid.space_order:
             raise ValueError("stencil order does not match grid order")
         L = _lib.lib()
@@ -197,6 +208,7 @@ class Solver:
         self._receiver_coordinates = []
         self._n_rec = 0
         self._verbose = False
+        self._verbose_quiet = False  # a slab rank other than 0 (SlabSolver): checks, no line
         self._loop_start = time.perf_counter()  # kernel.hpp:494 (reset by forward)
         self._snapshot_cap = 4 << 30
         self._prev = None
@@ -335,8 +347,9 @@ class Solver:
             if s % ci == 0 or s == total:
                 v = C.c_double()
                 _check(self._ctx, _lib.lib().fdw_max_abs(self._ctx, C.byref(v)), "fdw_max_abs")
-                sys.stderr.write("step %d/%d  %.3fs  max|p| = %.6e\n"
-                                 % (s, total, time.perf_counter() - self._loop_start, v.value))
+                if not self._verbose_quiet:
+                    sys.stderr.write("step %d/%d  %.3fs  max|p| = %.6e\n"
+                                     % (s, total, time.perf_counter() - self._loop_start, v.value))
 
     def _advance_raw(self, n: int, flags: int):
         bad_step = C.c_uint64()
