@@ -453,13 +453,7 @@ public:
                 check(fdw_download_seismogram(ctx_, result.seismogram.data.data(), n + 1),
                       "fdw_download_seismogram");
             } else {
-                // per-slab double partial sums, added in rank order, cast to T
-                // (acquisition.hpp:155-158 split at the slab faces)
-                std::vector<double> acc((n + 1) * n_receivers_, 0.0), part(acc.size());
-                for (auto* c : ctxs_) {
-                    check_ctx(fdw_download_seismogram_f64(c, part.data(), n + 1), c, "fdw_download_seismogram");
-                    for (std::size_t i = 0; i < acc.size(); ++i) acc[i] += part[i];
-                }
+                const std::vector<double> acc = merged_seismogram(n + 1);
                 for (std::size_t i = 0; i < acc.size(); ++i) result.seismogram.data[i] = static_cast<T>(acc[i]);
             }
         }
@@ -490,6 +484,46 @@ private:
             idx.push_back(0);
             w.push_back(0.0);
         }
+    }
+
+    // The seismogram of a slab decomposition, bit-identical to the
+    // reference's accumulation (acquisition.hpp:155-158): receivers inside
+    // one slab come from that rank's partial sum (the others hold 0); a
+    // receiver whose taps straddle a face is re-summed from every rank's
+    // per-tap products in entry order, sequentially from +0.0.
+    std::vector<double> merged_seismogram(std::size_t rows) {
+        std::vector<double> acc(rows * n_receivers_, 0.0), part(acc.size());
+        struct Tap {
+            uint64_t entry;
+            std::size_t rank, slot;
+        };
+        std::vector<std::vector<Tap>> split(n_receivers_);
+        std::vector<std::vector<double>> prod(ctxs_.size());
+        std::vector<uint64_t> nslot(ctxs_.size(), 0);
+        for (std::size_t r = 0; r < ctxs_.size(); ++r) {
+            check_ctx(fdw_download_seismogram_f64(ctxs_[r], part.data(), rows), ctxs_[r], "fdw_download_seismogram");
+            for (std::size_t i = 0; i < acc.size(); ++i) acc[i] += part[i];
+            check_ctx(fdw_receiver_split_info(ctxs_[r], &nslot[r], nullptr, nullptr), ctxs_[r], "fdw_receiver_split_info");
+            if (!nslot[r]) continue;
+            std::vector<uint64_t> rec(nslot[r]), ent(nslot[r]);
+            check_ctx(fdw_receiver_split_info(ctxs_[r], &nslot[r], rec.data(), ent.data()), ctxs_[r],
+                      "fdw_receiver_split_info");
+            prod[r].resize(rows * nslot[r]);
+            check_ctx(fdw_download_receiver_products(ctxs_[r], prod[r].data(), rows), ctxs_[r],
+                      "fdw_download_receiver_products");
+            for (std::size_t j = 0; j < nslot[r]; ++j) split[rec[j]].push_back({ent[j], r, j});
+        }
+        for (std::size_t p = 0; p < n_receivers_; ++p) {
+            auto& taps = split[p];
+            if (taps.empty()) continue;
+            std::sort(taps.begin(), taps.end(), [](const Tap& a, const Tap& b) { return a.entry < b.entry; });
+            for (std::size_t row = 0; row < rows; ++row) {
+                double s = 0.0;
+                for (const Tap& t : taps) s += prod[t.rank][row * nslot[t.rank] + t.slot];
+                acc[row * n_receivers_ + p] = s;
+            }
+        }
+        return acc;
     }
 
     static void check_ctx(fdw_status s, const fdw_solver* c, const char* what) {

@@ -197,6 +197,16 @@ fdw_status fdw_max_abs(fdw_solver* ctx, double* out);
 fdw_status fdw_download_seismogram(fdw_solver* ctx, void* out, uint64_t rows);
 fdw_status fdw_download_seismogram_f64(fdw_solver* ctx, double* out, uint64_t rows);
 
+/* Z slabs: receivers whose taps straddle a slab face keep per-tap products
+ * instead of a partial sum (their seismogram entries stay 0 on every rank), so
+ * the host can merge the ranks' products in entry order and sum them
+ * sequentially -- bit-identical to the reference's single accumulation
+ * (acquisition.hpp:155-158).  split_info: the number of product slots on this
+ * rank and, per slot, the receiver and the entry position within its
+ * InterpolationMap point (either array may be NULL).  products: rows x slots. */
+fdw_status fdw_receiver_split_info(fdw_solver* ctx, uint64_t* n_slots, uint64_t* receiver, uint64_t* entry);
+fdw_status fdw_download_receiver_products(fdw_solver* ctx, double* out, uint64_t rows);
+
 /* Waits for all work queued on the context (compute + copy streams); reports a
  * pending asynchronous instability like fdw_wait (without the step details). */
 fdw_status fdw_synchronize(fdw_solver* ctx);

@@ -87,6 +87,8 @@ _SIGS = {
     "fdw_peer_link": (C.c_int, [_P, _P, C.c_int32]),
     "fdw_peer_loopback": (C.c_int, [_P]),
     "fdw_debug_check_guards": (C.c_int, [_P, _U64P]),
+    "fdw_receiver_split_info": (C.c_int, [_P, _U64P, _U64P, _U64P]),
+    "fdw_download_receiver_products": (C.c_int, [_P, _P, C.c_uint64]),
 }
 
 FDW_PEER_BLOB_BYTES = 512

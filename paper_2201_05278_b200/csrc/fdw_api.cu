@@ -141,6 +141,12 @@ struct fdw_solver {
     unsigned int* d_rec_off = nullptr;
     double* d_rec_w = nullptr;
     double* d_seis = nullptr;
+    // slabs: taps of receivers that straddle a slab face -> per-tap products
+    int n_split = 0;                       // product slots on this rank
+    long long* d_sp_idx = nullptr;
+    double* d_sp_w = nullptr;
+    double* d_sp_prod = nullptr;           // [seis_rows][n_split]
+    std::vector<uint64_t> sp_rec, sp_entry; // per slot: receiver, entry position within it
     unsigned long long seis_rows = 0;
 
     unsigned long long host_step = 0;
@@ -1405,6 +1411,12 @@ fdw_status launch_peer_health(fdw_solver* c, int honor_abort) {
 template <typename T>
 fdw_status launch_receivers_t(fdw_solver* c, int lv, int row_add, cudaStream_t st) {
     if (c->n_rec == 0 || !c->d_seis) return FDW_OK;
+    if (c->n_split > 0) {
+        fdw::receiver_products_kernel<T><<<(c->n_split + 255) / 256, 256, 0, st>>>(
+            static_cast<const T*>(c->lvl[lv]), c->d_sp_idx, c->d_sp_w, c->d_sp_prod, c->n_split, c->seis_rows,
+            row_add, c->ctrl);
+        CHECK_LAUNCH();
+    }
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributePriority;
     attr[0].val.priority = c->prio_lo;  // below the step chain (launch_tma)
@@ -2574,6 +2586,8 @@ fdw_status fdw_destroy(fdw_solver* c) {
     for (void* p : {(void*)c->d_blk_toff, (void*)c->d_blk_tgt, (void*)c->d_blk_tpos, (void*)c->d_blk_roff,
                     (void*)c->d_blk_rpack, (void*)c->d_tap_ix, c->d_tapbuf})
         if (p) cudaFreeAsync(p, c->stream);
+    for (void* p : {(void*)c->d_sp_idx, (void*)c->d_sp_w, (void*)c->d_sp_prod})
+        if (p) cudaFreeAsync(p, c->stream);
     for (void* p : {(void*)c->d_eidx, (void*)c->d_etab})
         if (p) cudaFreeAsync(p, c->stream);
     for (void* p : {(void*)c->d_ezr, (void*)c->ctrl, (void*)c->d_tgt, (void*)c->d_ent_off, (void*)c->d_ent_w, (void*)c->d_wavelet,
@@ -2895,21 +2909,44 @@ fdw_status fdw_set_receivers(fdw_solver* c, uint64_t n_points, const uint64_t* o
                              const double* w) {
     fdw_status s = enter(c);
     if (s) return s;
-    std::vector<long long> ri;
+    std::vector<long long> ri, si;
     std::vector<unsigned int> ro(1, 0);
-    std::vector<double> rw;
+    std::vector<double> rw, sw;
+    c->sp_rec.clear();
+    c->sp_entry.clear();
     for (uint64_t p = 0; p < n_points; ++p) {
+        uint64_t kept = 0;
+        for (uint64_t e = off[p]; e < off[p + 1]; ++e) kept += remap(c, idx[e]) >= 0;
+        // a receiver with taps on this and another slab: per-tap products
+        const bool split = c->d.world > 1 && kept > 0 && kept < off[p + 1] - off[p];
         for (uint64_t e = off[p]; e < off[p + 1]; ++e) {
             const long long o = remap(c, idx[e]);
             if (o < 0) continue;
-            ri.push_back(o);
-            rw.push_back(w[e]);
+            if (split) {
+                si.push_back(o);
+                sw.push_back(w[e]);
+                c->sp_rec.push_back(p);
+                c->sp_entry.push_back(e - off[p]);
+            } else {
+                ri.push_back(o);
+                rw.push_back(w[e]);
+            }
         }
         ro.push_back((unsigned int)ri.size());
     }
     if ((s = dev_upload(c, &c->d_rec_idx, ri))) return s;
     if ((s = dev_upload(c, &c->d_rec_off, ro))) return s;
     if ((s = dev_upload(c, &c->d_rec_w, rw))) return s;
+    if ((s = dev_upload(c, &c->d_sp_idx, si))) return s;
+    if ((s = dev_upload(c, &c->d_sp_w, sw))) return s;
+    c->n_split = (int)si.size();
+    if (c->d_sp_prod) cudaFreeAsync(c->d_sp_prod, c->stream);
+    c->d_sp_prod = nullptr;
+    if (c->n_split) {
+        const size_t bytes = (size_t)(c->d.n_steps + 1) * c->n_split * sizeof(double);
+        CU(cudaMallocAsync(reinterpret_cast<void**>(&c->d_sp_prod), bytes, c->stream));
+        CU(cudaMemsetAsync(c->d_sp_prod, 0, bytes, c->stream));
+    }
     if (c->res2d && (s = res2d_receivers(c, ri))) return s;
     if (c->d_seis) cudaFreeAsync(c->d_seis, c->stream);
     c->d_seis = nullptr;
@@ -3139,6 +3176,28 @@ fdw_status fdw_download_seismogram_f64(fdw_solver* c, double* out, uint64_t rows
     if (rows > c->seis_rows) return fail(c, FDW_EINVAL, "rows exceed the seismogram");
     if (c->n_rec == 0 || rows == 0) return FDW_OK;
     CU(cudaMemcpyAsync(out, c->d_seis, (size_t)rows * c->n_rec * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return FDW_OK;
+}
+
+fdw_status fdw_receiver_split_info(fdw_solver* c, uint64_t* n_slots, uint64_t* receiver, uint64_t* entry) {
+    fdw_status s = prologue(c);
+    if (s) return s;
+    if (!n_slots) return fail(c, FDW_EINVAL, "null output");
+    *n_slots = (uint64_t)c->n_split;
+    if (receiver) std::copy(c->sp_rec.begin(), c->sp_rec.end(), receiver);
+    if (entry) std::copy(c->sp_entry.begin(), c->sp_entry.end(), entry);
+    return FDW_OK;
+}
+
+fdw_status fdw_download_receiver_products(fdw_solver* c, double* out, uint64_t rows) {
+    fdw_status s = enter(c);
+    if (s) return s;
+    if (rows > c->seis_rows) return fail(c, FDW_EINVAL, "rows exceed the seismogram");
+    if (c->n_split == 0 || rows == 0) return FDW_OK;
+    if (c->side) CU(cudaStreamSynchronize(c->side));
+    CU(cudaMemcpyAsync(out, c->d_sp_prod, (size_t)rows * c->n_split * sizeof(double), cudaMemcpyDeviceToHost,
                        c->stream));
     CU(cudaStreamSynchronize(c->stream));
     return FDW_OK;

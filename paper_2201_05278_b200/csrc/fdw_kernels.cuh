@@ -2430,6 +2430,23 @@ __global__ void __launch_bounds__(32 * REC_WARPS)
     if (lane == 0) seis[row * (unsigned long long)n_rec + r] = acc;
 }
 
+// Receivers whose taps straddle a slab face (Z slabs): the reference sums a
+// receiver's products in entry order in ONE sequential double accumulation
+// (acquisition.hpp:155-158), which per-slab partial sums cannot reproduce.
+// For those taps each rank stores the products themselves, row by row; the
+// host merges the ranks' products in entry order and sums them sequentially,
+// so the seismogram stays bit-identical to the reference at any slab count.
+template <typename T>
+__global__ void receiver_products_kernel(const T* __restrict__ u, const long long* __restrict__ idx,
+                                         const double* __restrict__ w, double* prod, int n_slots,
+                                         unsigned long long n_rows, int row_add, const Ctrl* ctrl) {
+    if (ctrl->abort) return;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long row = ctrl->step + (unsigned long long)row_add - ctrl->row_base;
+    if (j >= n_slots || row >= n_rows) return;
+    prod[row * (unsigned long long)n_slots + j] = __dmul_rn(w[j], static_cast<double>(u[idx[j]]));
+}
+
 // max_abs / check_health, kernel.hpp:265-273 and :456-458.  max |u| over
 // finite values plus the smallest global padded flat index holding a
 // non-finite value (the reference returns the first one in flat order).

@@ -6,7 +6,8 @@ halo epochs in per-rank sync blocks (fdw_api.cu enqueue_step).  This module only
 does the control-plane work around it with torch.distributed:
   * all-gather the peer IPC blobs (link_peers),
   * build each rank's slab workload (configs.build_workload(rank, world)),
-  * reduce per-rank partial seismograms in rank order (double) and cast to T,
+  * merge per-rank seismograms exactly (partials + straddling receivers'
+    per-tap products in entry order) and cast to T,
   * gather halo-stripped slabs for checking.
 """
 from __future__ import annotations
@@ -35,10 +36,55 @@ def slab_range(n_ext: int, world: int, rank: int) -> tuple:
     return int(b.value), int(e.value)
 
 
+def split_products(solver, rows: int):
+    """This rank's per-tap products of the receivers that straddle a slab face
+    (fdw_receiver_split_info / fdw_download_receiver_products): (receiver,
+    entry position, products[rows, slots])."""
+    L = _lib.lib()
+    n = C.c_uint64()
+    L.fdw_receiver_split_info(solver.ctx, C.byref(n), None, None)
+    m = int(n.value)
+    rec = np.zeros(max(m, 1), np.uint64)
+    ent = np.zeros(max(m, 1), np.uint64)
+    prod = np.zeros((rows, max(m, 1)), np.float64)
+    if m:
+        u64 = C.POINTER(C.c_uint64)
+        L.fdw_receiver_split_info(solver.ctx, C.byref(n), rec.ctypes.data_as(u64), ent.ctypes.data_as(u64))
+        rc = L.fdw_download_receiver_products(solver.ctx, _lib.ptr(prod), rows)
+        if rc != 0:
+            raise RuntimeError("fdw_download_receiver_products failed")
+    return rec[:m], ent[:m], prod[:, :m]
+
+
+def merge_seismogram(partials, splits, n_rec: int) -> np.ndarray:
+    """The seismogram (rows x receivers, double) of a slab decomposition, bit-
+    identical to the reference's single-domain accumulation
+    (acquisition.hpp:155-158): receivers inside one slab come from that
+    rank's partial sum (the other ranks hold 0 for them); a receiver whose
+    taps straddle a face is recomputed from every rank's per-tap products in
+    entry order, summed sequentially from +0.0 (np.add.accumulate is a
+    left-to-right running sum)."""
+    acc = np.asarray(partials[0], np.float64).reshape(-1, n_rec).copy()
+    for p in partials[1:]:
+        acc += np.asarray(p, np.float64).reshape(-1, n_rec)
+    cols = {}
+    for r, (rec, ent, prod) in enumerate(splits):
+        for j in range(len(rec)):
+            cols.setdefault(int(rec[j]), []).append((int(ent[j]), r, j))
+    rows = acc.shape[0]
+    for p, lst in cols.items():
+        lst.sort()
+        m = np.zeros((rows, len(lst) + 1), np.float64)
+        for k, (_, r, j) in enumerate(lst):
+            m[:, k + 1] = splits[r][2][:rows, j]
+        acc[:, p] = np.add.accumulate(m, axis=1)[:, -1]
+    return acc.reshape(-1)
+
+
 def reduce_seismogram(partial: np.ndarray, dtype, group=None) -> np.ndarray:
-    """Sum of per-rank double partials in rank order (rank 0 first), cast to T.
-    For world == 1 this is the reference's own accumulation (acquisition.hpp:
-    155-158); for world > 1 the per-receiver sum is split at slab faces."""
+    """Sum of per-rank double partials in rank order (rank 0 first), cast to T
+    (exact only for receivers inside one slab; gather_seismogram is exact
+    everywhere).  Collective."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -49,6 +95,18 @@ def reduce_seismogram(partial: np.ndarray, dtype, group=None) -> np.ndarray:
     for p in parts[1:]:
         acc += p.numpy()
     return acc.astype(dtype)
+
+
+def gather_seismogram(solver, dtype, group=None, rows=None) -> np.ndarray:
+    """The whole seismogram of a slab decomposition on every rank of `group`,
+    cast to T: per-rank partials plus the straddling receivers' per-tap
+    products, merged exactly (merge_seismogram).  Collective."""
+    import torch.distributed as dist
+    rows = solver.time_axis().n_steps + 1 if rows is None else rows
+    mine = (solver.seismogram_f64(rows), split_products(solver, rows))
+    parts = [None] * dist.get_world_size(group)
+    dist.all_gather_object(parts, mine, group=group)
+    return merge_seismogram([p[0] for p in parts], [p[1] for p in parts], solver._n_rec).astype(dtype)
 
 
 def gather_slabs(local_ext: np.ndarray, group=None) -> np.ndarray:

@@ -223,10 +223,10 @@ class SlabSolver:
 
     # -- device-side extras --
     def seismogram_f64(self, rows: Optional[int] = None) -> np.ndarray:
-        """Per-slab double partial sums, added in rank order
-        (acquisition.hpp:155-158, split at the slab faces)."""
-        acc = None
-        for s in self._ranks:
-            p = s.seismogram_f64(rows)
-            acc = p.copy() if acc is None else acc + p
-        return acc
+        """The reference's accumulation (acquisition.hpp:155-158) over all
+        slabs, bit for bit: per-slab partials plus the straddling receivers'
+        per-tap products merged in entry order (dist.merge_seismogram)."""
+        from .dist import merge_seismogram, split_products
+        rows = self._time.n_steps + 1 if rows is None else rows
+        parts = [s.seismogram_f64(rows) for s in self._ranks]
+        return merge_seismogram(parts, [split_products(s, rows) for s in self._ranks], self._n_rec)

@@ -23,6 +23,7 @@ def test_bench_two_ranks_emulated(workload, scaling):
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["scaling"] == scaling
     assert line["config"]["workload"] == ("C5" if workload == "auto" else "C4")
-    assert line["parity"]["ok"] and line["parity"]["field_bit_exact"], line["parity"]
+    assert line["parity"]["ok"] and line["parity"]["field_bit_exact"] and line["parity"]["seismogram_bit_exact"], \
+        line["parity"]
     assert "host-ordered" in line["transport"]
     assert line["value"] > 0 and line["gpu_launches"] > 0

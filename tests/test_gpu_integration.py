@@ -32,7 +32,7 @@ def _model(d, name, arr, units):
     return {"path": os.path.join(d, name + ".bin"), "sidecar": os.path.join(d, name + ".json")}
 
 
-def _config(d, ndim, dtype, stride, density, dt=None):
+def _config(d, ndim, dtype, stride, density, dt=None, rec_z=25.0):
     if ndim == 2:
         shape, bbox, h = (41, 61), [0, 400, 0, 600], [10.0, 10.0]
         src, recs = [[45.0, 305.0]], [[25.0, 15.0 + 20.0 * k] for k in range(25)]
@@ -40,7 +40,7 @@ def _config(d, ndim, dtype, stride, density, dt=None):
         damping = [0, 100, 100, 100]
     else:
         shape, bbox, h = (21, 31, 26), [0, 200, 0, 300, 0, 250], [10.0, 10.0, 10.0]
-        src, recs = [[45.0, 155.0, 125.0]], [[25.0, 15.0 + 20.0 * k, 125.0] for k in range(12)]
+        src, recs = [[45.0, 155.0, 125.0]], [[rec_z, 15.0 + 20.0 * k, 125.0] for k in range(12)]
         bc = ["null_neumann", "null_dirichlet", "null_dirichlet", "null_dirichlet", "none", "null_dirichlet"]
         damping = [0, 50, 50, 50, 50, 50]
     iz = np.arange(shape[0]).reshape((-1,) + (1,) * (ndim - 1))
@@ -96,15 +96,16 @@ def test_run_artifacts_identical_to_the_cpu_reference(tmp_path, ndim, dtype, str
             assert open(os.path.join(a, f), "rb").read() == open(os.path.join(b, f), "rb").read(), f
 
 
-@pytest.mark.parametrize("devices,dtype,stride,density", [
-    ("0,0", "float32", 25, True), ("0,0,0", "float64", 0, False)])
-def test_run_on_slabs_identical_to_the_cpu_reference(tmp_path, devices, dtype, stride, density):
+@pytest.mark.parametrize("devices,dtype,stride,density,rec_z", [
+    ("0,0", "float32", 25, True, 25.0), ("0,0,0", "float64", 0, False, 25.0), ("0,0", "float32", 0, False, 125.0),
+    ("0,0,0", "float64", 20, False, 95.0)])
+def test_run_on_slabs_identical_to_the_cpu_reference(tmp_path, devices, dtype, stride, density, rec_z):
     """The reference's unmodified runner.hpp `Solver<T> solver(...)` spread over
     several GPUs (FDW_DEVICES: Z slabs, halo planes over peer memory), here
     emulated on one GPU: every artefact must still be byte-identical to the CPU
-    reference (the receivers lie inside the first slab, so their double sums
-    are not split)."""
-    cfg = _config(str(tmp_path), 3, dtype, stride, density)
+    reference -- also with the receiver line across a slab face (rec_z 125 m /
+    95 m: taps on two slabs, merged from per-tap products in entry order)."""
+    cfg = _config(str(tmp_path), 3, dtype, stride, density, rec_z=rec_z)
     a = str(tmp_path / "cpu")
     assert _run(_exe("fdwave_cpu"), cfg, a).returncode == 0
     b = str(tmp_path / "cuda")
