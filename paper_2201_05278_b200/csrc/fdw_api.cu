@@ -1863,6 +1863,11 @@ fdw_status read_ctrl(fdw_solver* c) {
 // Picks the Z-segment count for the Z-march kernel: fill whole waves of
 // resident CTAs while keeping the 2R-plane queue warm-up small.
 int pick_zseg(fdw_solver* c, int occ) {
+    // Thin slabs (strong scaling): 3 segments measured best at 27, 54 and 109
+    // planes of C4 (middle ranks with emulated neighbours, split-ring sweep:
+    // 93 / 149 / 261 us against 103 / 159 / 267 us for this model's pick,
+    // tools/strong_probe.py, profiles/r02/strong_probe.json).
+    if (c->nzl <= 128) return (int)std::max<long long>(1, std::min<long long>(3, c->nzl / c->R));
     // Cost model in units of plane-steps of one CTA, fitted on B200 (C4 and C3
     // sweeps over 4..14 segments): a segment of n planes costs n + 0.2*2R
     // (queue warm-up); the grid drains at `resident` CTAs; half a CTA of tail
