@@ -614,7 +614,8 @@ def run_reference(args):
         return None
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
-    wname, cfg = workload_cfg(args.workload, 1)
+    # the same workload as our arm at this N (C5 at N > 1 is 200 planes per GPU)
+    wname, cfg = workload_cfg(args.workload, max(world, args.gpus))
     if O.rlib() is None:
         return {"impl": "reference", "unavailable": "oracle/_ref/libfdwave_ref.so not built"}
     t0 = time.time()
