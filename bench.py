@@ -581,13 +581,15 @@ def cpu_baseline(cfg, seconds, states=None, wname=None, n_steps=None):
                            f"reference Solver<float> Backend::Parallel; setup {setup:.1f} s excluded",
                "per_state_gpts": {k: round(pts * v[0] / v[1] / 1e9, 4) for k, v in samples.items()},
                "cpu_model": _cpu_model()}
-        full = os.path.join(ROOT, "tests", "golden", f"full_{(wname or '').lower()}.npz")
+        # the whole forward, measured once on a GPU box of this pool next to a
+        # bench line (tools/cpu_full_run.py; bit-identical to the fixtures)
+        full = os.path.join(ROOT, "profiles", "r02", f"cpu_full_{(wname or '').lower()}.json")
         if os.path.exists(full):
-            import json as _json
-            m = _json.loads(str(np.load(full)["meta"]))
-            out["full_run"] = {"gpts": round(m["gpts_per_s"], 4), "seconds": round(m["seconds"], 1),
-                               "steps": m["n_steps"], "threads": m["threads"],
-                               "where": "build container (not this host), oracle/gen_fullsize.py"}
+            with open(full) as f:
+                m = json.load(f)
+            out["full_run"] = {"gpts": m["gpts"], "seconds": m["kernel_seconds"], "steps": m["n_steps"],
+                               "threads": m["threads"], "bit_identical_to_fixture": m["matches_fixture"],
+                               "where": f"GPU box of this pool, earlier run ({os.path.relpath(full, ROOT)})"}
         return out
     except Exception as e:  # keep the GPU line valid
         return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
