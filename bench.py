@@ -636,7 +636,8 @@ def run_reference(args):
     return {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if max(world, args.gpus) > 1 and wname in ("C3", "C4") else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": wname, "name": cfg.name, "extended_shape": list(run.extended),
                    "step": f"{per} reference time steps (bounded sample of the forward run)",
                    "setup_seconds": round(setup, 2)},
