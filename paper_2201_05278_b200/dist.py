@@ -81,10 +81,12 @@ def merge_seismogram(partials, splits, n_rec: int) -> np.ndarray:
     return acc.reshape(-1)
 
 
-def reduce_seismogram(partial: np.ndarray, dtype, group=None) -> np.ndarray:
-    """Sum of per-rank double partials in rank order (rank 0 first), cast to T
-    (exact only for receivers inside one slab; gather_seismogram is exact
-    everywhere).  Collective."""
+def reduce_partials(partial: np.ndarray, dtype, group=None) -> np.ndarray:
+    """Sum of per-rank double partial sums in rank order (rank 0 first), cast
+    to T -- for partials that carry ALL of a rank's taps (the numpy emulation
+    of test_slabs_gloo.py).  A library slab Solver keeps the taps of
+    receivers that straddle a face as products instead (its partial holds 0
+    there): use gather_seismogram for it.  Collective."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -123,3 +125,6 @@ def gather_slabs(local_ext: np.ndarray, group=None) -> np.ndarray:
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad, group=group)
     return np.concatenate([p[: int(s.item())].numpy() for p, s in zip(parts, sizes)], axis=0)
+
+
+reduce_seismogram = gather_seismogram  # the library path: exact at any slab count

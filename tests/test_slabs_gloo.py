@@ -135,7 +135,7 @@ def _worker(rank, world, port, cfg, q):
             exchange(curr)
             record(n + 1, curr)
         full = fdist.gather_slabs(curr[h:L - h, h:P1 - h, h:P2 - h])
-        sg = fdist.reduce_seismogram(seis, np.float64)
+        sg = fdist.reduce_partials(seis, np.float64)
         if rank == 0:
             q.put((full, sg, np.asarray(w.velocity), (zb, ze)))
     finally:
