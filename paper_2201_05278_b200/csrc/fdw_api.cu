@@ -30,10 +30,18 @@
 #include <unistd.h>
 
 #include "../../include/fdwave_cuda.h"
+#include "fdw_inst.h"
 #include "fdw_kernels.cuh"
 
 using fdw::Ctrl;
 using fdw::SweepArgs;
+using fdwi::TMA_BX;
+using fdwi::TMA_PD;
+using fdwi::tma_kernel;
+using fdwi::tma_vd_kernel;
+using fdwi::fused2d_kernel;
+using fdwi::res2d_kernel;
+using fdwi::res2d2_kernel;
 
 namespace {
 
@@ -524,14 +532,6 @@ bool launch_zmarch(fdw_solver* c, const SweepArgs<T>& a) {
 
 bool zmarch_supported(int R) { return R == 1 || R == 2 || R == 4; }
 
-constexpr int TMA_BX = 16;
-
-template <typename T, int R, bool EX, int MINB>
-const void* tma_fn() {
-    return (const void*)fdw::sweep3d_tma<T, R, TMA_BX, EX, MINB>;
-}
-
-constexpr int TMA_PD = 2;  // split-ring prefetch depth (FDW_TMA_PD=2)
 
 template <typename T>
 int tma_smem(int R, bool vd = false, int pd = 0) {
@@ -561,67 +561,6 @@ int tma_smem(int R, bool vd = false, int pd = 0) {
         case 2: return fdw::TmaShape<T, 2, TMA_BX>::SMEM;
         default: return fdw::TmaShape<T, 4, TMA_BX>::SMEM;
     }
-}
-
-// variable-density TMA sweep (2 CTAs/SM: 6 tiles per plane stage)
-template <typename T>
-const void* tma_vd_kernel(int R, bool ex, bool fast = false) {
-    if constexpr (std::is_same<T, float>::value) {
-        if (fast) {  // split rings + damping table
-#define TKVF(RR) \
-    if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 2, true, TMA_PD, true> \
-                           : (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, false, 2, true, TMA_PD, true>;
-            TKVF(1)
-            TKVF(2)
-            TKVF(4)
-#undef TKVF
-            return nullptr;
-        }
-    }
-#define TKV(RR) \
-    if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 2, true> \
-                           : (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, false, 2, true>;
-    TKV(1)
-    TKV(2)
-    TKV(4)
-#undef TKV
-    return nullptr;
-}
-
-// minb: 2 or 3 resident CTAs requested from ptxas (register cap 128 / 80)
-template <typename T>
-const void* tma_kernel(int R, bool ex, int minb, int pd = 0, bool etab = false) {
-    if constexpr (std::is_same<T, float>::value) {
-        if (pd > 0 && etab) {  // split rings with the damping table
-#define TKE(RR) \
-    if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 3, false, TMA_PD, true> \
-                           : (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, false, 3, false, TMA_PD, true>;
-            TKE(1)
-            TKE(2)
-            TKE(4)
-#undef TKE
-            return nullptr;
-        }
-    }
-    if (pd > 0) {  // split rings: 3 CTAs/SM only
-#define TKP(RR) \
-    if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 3, false, TMA_PD> \
-                           : (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, false, 3, false, TMA_PD>;
-        TKP(1)
-        TKP(2)
-        TKP(4)
-#undef TKP
-        return nullptr;
-    }
-#define TK(RR)                                                                                  \
-    if (R == RR)                                                                                \
-        return ex ? (minb == 3 ? tma_fn<T, RR, true, 3>() : tma_fn<T, RR, true, 2>())            \
-                  : (minb == 3 ? tma_fn<T, RR, false, 3>() : tma_fn<T, RR, false, 2>());
-    TK(1)
-    TK(2)
-    TK(4)
-#undef TK
-    return nullptr;
 }
 
 fdw::PeerArgs peer_args(fdw_solver* c);
@@ -687,91 +626,27 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    auto go = [&](auto kern) {
-        // an error is left for the caller's CHECK_LAUNCH (cudaGetLastError)
-        // tm_p[src]: the split rings' head tile (interior box on the current level);
-        // with the damping table the eta stream is the 1-byte index map
-        (void)cudaLaunchKernelEx(&cfg, kern, a, c->tm_u[src], c->tm_p[dst], c->tm_c, etab ? c->tm_eb : c->tm_e, g0,
-                                 g1, g2, c->tm_p[src], col_base);
-        return true;
-    };
-
-    switch (c->R) {
-#define LT(RR)                                                                 \
-    case RR:                                                                   \
-        if (c->vd && etab) {                                                   \
-            if constexpr (std::is_same<T, float>::value)                       \
-                return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2, true, TMA_PD, true>); \
-            return false;                                                      \
-        }                                                                      \
-        if (c->vd) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2, true>);   \
-        if (pd > 0 && etab) {                                                  \
-            if constexpr (std::is_same<T, float>::value)                       \
-                return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3, false, TMA_PD, true>); \
-            return false;                                                      \
-        }                                                                      \
-        if (pd > 0) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3, false, TMA_PD>); \
-        if (c->tma_minb == 3) return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 3>); \
-        return go(fdw::sweep3d_tma<T, RR, TMA_BX, EX, 2>);
-        LT(1)
-        LT(2)
-        LT(4)
-#undef LT
-        default: return false;
+    if (c->R != 1 && c->R != 2 && c->R != 4) return false;
+    constexpr bool F32 = std::is_same<T, float>::value;
+    const void* kern = nullptr;
+    if (c->vd) {
+        if (etab && !F32) return false;
+        kern = tma_vd_kernel<T>(c->R, EX, etab);
+    } else if (pd > 0) {
+        if (etab && !F32) return false;
+        kern = tma_kernel<T>(c->R, EX, 3, pd, etab);
+    } else {
+        kern = tma_kernel<T>(c->R, EX, c->tma_minb == 3 ? 3 : 2);
     }
-}
-
-template <typename T, bool EX>
-const void* fused2d_fn(int R) {
-#define F2(RR) \
-    if (R == RR) return (const void*)fdw::step2d_fused<T, RR, EX>;
-    F2(1) F2(2) F2(3) F2(4) F2(5) F2(6) F2(7) F2(8) F2(9) F2(10)
-#undef F2
-    return nullptr;
-}
-
-// variable density: exact arithmetic only (FMA mode falls back to SIMPLE)
-template <typename T>
-const void* fused2d_vd_fn(int R) {
-#define F2V(RR) \
-    if (R == RR) return (const void*)fdw::step2d_fused<T, RR, true, true>;
-    F2V(1) F2V(2) F2V(3) F2V(4) F2V(5) F2V(6) F2V(7) F2V(8) F2V(9) F2V(10)
-#undef F2V
-    return nullptr;
-}
-
-template <typename T>
-const void* fused2d_kernel(int R, bool ex, bool vd = false) {
-    if (vd) return ex ? fused2d_vd_fn<T>(R) : nullptr;
-    return ex ? fused2d_fn<T, true>(R) : fused2d_fn<T, false>(R);
-}
-
-template <typename T, bool EX>
-const void* res2d_fn(int R) {
-#define RF(RR) \
-    if (R == RR) return (const void*)fdw::step2d_resident<T, RR, EX>;
-    RF(1) RF(2) RF(3) RF(4) RF(5) RF(6) RF(7) RF(8) RF(9) RF(10)
-#undef RF
-    return nullptr;
-}
-
-template <typename T>
-const void* res2d_kernel(int R, bool ex) {
-    return ex ? res2d_fn<T, true>(R) : res2d_fn<T, false>(R);
-}
-
-template <typename T, bool EX>
-const void* res2d2_fn(int R) {
-#define RF2(RR) \
-    if (R == RR) return (const void*)fdw::step2d_resident2<T, RR, EX>;
-    RF2(1) RF2(2) RF2(3) RF2(4) RF2(5) RF2(6) RF2(7) RF2(8) RF2(9) RF2(10)
-#undef RF2
-    return nullptr;
-}
-
-template <typename T>
-const void* res2d2_kernel(int R, bool ex) {
-    return ex ? res2d2_fn<T, true>(R) : res2d2_fn<T, false>(R);
+    if (!kern) return false;
+    // an error is left for the caller's CHECK_LAUNCH (cudaGetLastError)
+    // tm_p[src]: the split rings' head tile (interior box on the current level);
+    // with the damping table the eta stream is the 1-byte index map
+    CUtensorMap maps[8] = {c->tm_u[src], c->tm_p[dst], c->tm_c, etab ? c->tm_eb : c->tm_e, g0, g1, g2, c->tm_p[src]};
+    int cb = col_base;
+    void* args[10] = {&a, &maps[0], &maps[1], &maps[2], &maps[3], &maps[4], &maps[5], &maps[6], &maps[7], &cb};
+    (void)cudaLaunchKernelExC(&cfg, kern, args);
+    return true;
 }
 
 size_t res2d2_smem(const fdw_solver* c, int BZ, int tapcap) {

@@ -16,7 +16,10 @@
 
 #include <type_traits>
 
+// Internal linkage: every translation unit that includes this header (fdw_api.cu,
+// fdw_inst_*.cu) owns its copies; kernels cross TUs only as host stubs.
 namespace fdw {
+namespace {
 
 // ---------------------------------------------------------------------------
 // Device control block: step counter, abort latch, health-check scratch.
@@ -2765,4 +2768,5 @@ __global__ void c2dt2_kernel(T* f, unsigned long long n, double dt) {
     f[t] = static_cast<T>(__dmul_rn(__dmul_rn(__dmul_rn(cv, cv), dt), dt));
 }
 
+}  // namespace
 }  // namespace fdw
