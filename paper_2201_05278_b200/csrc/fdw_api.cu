@@ -227,6 +227,7 @@ struct fdw_solver {
     size_t res_smem_base = 0;
     void* d_tapbuf = nullptr;
     int n_ent = 0;
+    void* d_res_hbuf = nullptr;  // two-step resident 2D kernel: strip buffers (2 levels)
     // peer transport (Z slabs, world > 1): halo planes stored straight into
     // the neighbours' levels over NVLink, halo epochs and the health reduction
     // through per-rank sync blocks
@@ -699,6 +700,8 @@ fdw_status launch_res2d_t(fdw_solver* c, int L, int cur0, bool record) {
     int rec = record && c->d_seis && c->d_tapbuf ? 1 : 0;
     const bool ex = c->d.math == FDW_MATH_EXACT;
     int Lp = c->res_pair ? (L & ~1) : 0, k0 = 0;
+    a.hbuf[0] = static_cast<T*>(c->d_res_hbuf);
+    a.hbuf[1] = a.hbuf[0] + c->level_elems;
     if (Lp >= 2) {  // pairs of steps, one grid barrier each
         void* args2[] = {&a, &Lp, &cur0, &rec};
         const void* f2 = res2d2_kernel<T>(c->R, ex);
@@ -766,6 +769,13 @@ bool res2d_configure(fdw_solver* c) {
                 continue;
             }
             if ((long long)zbn * xb > (long long)got * c->sm_count) continue;
+            const size_t hb = 2 * c->level_elems * sizeof(T);
+            if (cudaMalloc(&c->d_res_hbuf, hb) != cudaSuccess || cudaMemset(c->d_res_hbuf, 0, hb) != cudaSuccess) {
+                cudaGetLastError();
+                if (c->d_res_hbuf) cudaFree(c->d_res_hbuf);
+                c->d_res_hbuf = nullptr;
+                break;  // the one-step kernel below
+            }
             c->res2d = true;
             c->res_pair = true;
             c->res_BZ = BZ;
@@ -2466,6 +2476,7 @@ fdw_status fdw_destroy(fdw_solver* c) {
     for (void* p : {(void*)c->d_blk_toff, (void*)c->d_blk_tgt, (void*)c->d_blk_tpos, (void*)c->d_blk_roff,
                     (void*)c->d_blk_rpack, (void*)c->d_tap_ix, c->d_tapbuf})
         if (p) cudaFreeAsync(p, c->stream);
+    if (c->d_res_hbuf) cudaFree(c->d_res_hbuf);
     for (void* p : {(void*)c->d_sp_idx, (void*)c->d_sp_w, (void*)c->d_sp_prod})
         if (p) cudaFreeAsync(p, c->stream);
     for (void* p : {(void*)c->d_eidx, (void*)c->d_etab})

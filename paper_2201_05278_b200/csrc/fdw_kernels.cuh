@@ -1324,6 +1324,9 @@ struct Res2DArgs {
     int n_rec;
     unsigned long long n_rows;
     Ctrl* ctrl;
+    // two-step kernel only: strip / halo exchange buffers (level-shaped, same
+    // origin and pitch as the levels), alternated by pair parity
+    T* hbuf[2];
 };
 
 // block-local coordinates (rr, cc in [-512, 1536)) packed into 22 bits
@@ -1944,8 +1947,11 @@ __global__ void __launch_bounds__(256, 2) step2d_resident2(Res2DArgs<T> a, int L
         __syncthreads();
         inject(sU, n1 + 1, false);
         // 2R-wide strips of the newest level; receiver taps of both rows
+        // The strips go to a buffer the chunk-start loads never read, and pair j
+        // uses buffer j & 1: a block overwrites pair j's strips only in pair
+        // j + 2, after the barrier its neighbours reach once they loaded them.
         {
-            T* g = a.lvl[cur0];
+            T* g = a.hbuf[(k >> 1) & 1];
             for (int i = tid; i < 2 * R * TX; i += 256) {
                 const int rr = i / TX, cc = i % TX;
                 if (cc >= bx) continue;
@@ -2016,7 +2022,7 @@ __global__ void __launch_bounds__(256, 2) step2d_resident2(Res2DArgs<T> a, int L
         // L2 loads in batches before storing any of them, and the first batch
         // is in flight during the previous pair's receiver sums.
         {
-            const T* g = a.lvl[cur0];
+            const T* g = a.hbuf[(k >> 1) & 1];
             constexpr int UWV = UW / V, H2V = H2 / V, B = 2;
             const int n_rows = 2 * R * UWV, n_tot = 2 * n_rows + bz * 2 * H2V;
             for (int i0 = 0; i0 < n_tot; i0 += B * 256) {
