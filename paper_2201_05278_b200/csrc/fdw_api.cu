@@ -250,7 +250,7 @@ struct fdw_solver {
     bool loopback = false;
     // timing experiments (tools/peer_overhead.py), read at create: FDW_DBG_NO_SEGROT,
     // FDW_DBG_NO_HALO_STORE (loopback only), FDW_DBG_FENCE_ALL
-    bool dbg_no_rot = false, dbg_no_store = false, dbg_fence_all = false;
+    bool dbg_no_rot = false, dbg_no_store = false, dbg_fence_all = false, dbg_fence_sc = false;
     void* loop_lvl[2] = {nullptr, nullptr};
     fdw::PeerSync* loop_sync = nullptr;
 };
@@ -596,7 +596,7 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
         a.n_bnd = nseg * grid.x * grid.y;
         a.seg_rot = c->dbg_no_rot ? 0 : S - 1;
         a.halo_store = c->loopback && c->dbg_no_store ? 0 : 1;
-        a.fence_all = c->dbg_fence_all ? 1 : 0;
+        a.fence_all = c->dbg_fence_all ? 1 : c->dbg_fence_sc ? 2 : 0;
     }
     const int col_base = (int)(c->base + c->R);
     const bool etab = c->tma_pd > 0 && c->n_etab > 0;
@@ -2315,6 +2315,7 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
     c->dbg_no_rot = std::getenv("FDW_DBG_NO_SEGROT") != nullptr;
     c->dbg_no_store = std::getenv("FDW_DBG_NO_HALO_STORE") != nullptr;
     c->dbg_fence_all = std::getenv("FDW_DBG_FENCE_ALL") != nullptr;
+    c->dbg_fence_sc = std::getenv("FDW_DBG_FENCE_SC") != nullptr;
     if (!std::getenv("FDW_NO_PRIO")) {
         int lo = 0, hi = 0;
         if (cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess) {

@@ -96,6 +96,10 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ unsigned int ld_volatile_u32(const unsigned int* p) {
     return *reinterpret_cast<const volatile unsigned int*>(p);
 }
+// Release/acquire fence at system scope (MEMBAR.ALL.SYS).  __threadfence_system()
+// emits the sequentially consistent MEMBAR.SC.SYS, which the message-passing
+// patterns here (stores, fence, flag) do not need and which costs far more.
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long global_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -154,7 +158,7 @@ __device__ __forceinline__ bool peer_wait_neighbours(const PeerArgs& p) {
 __device__ __forceinline__ void peer_publish(const PeerArgs& p) {
     const unsigned long long e = p.self->halo_epoch + 1;
     p.self->halo_epoch = e;
-    __threadfence_system();
+    fence_acq_rel_sys();
     if (p.rank > 0) st_release_sys(&p.peer[p.rank - 1]->halo_flag[p.rank], e);
     if (p.rank < p.world - 1) st_release_sys(&p.peer[p.rank + 1]->halo_flag[p.rank], e);
 }
@@ -278,7 +282,7 @@ struct SweepArgs {
     unsigned int n_bnd;
     int publish;
     int halo_store;  // 0: skip the halo stores (fdw_peer_loopback timing experiments only)
-    int fence_all;   // 1: every thread fences its stores (A/B of the one-fence-per-CTA release)
+    int fence_all;   // A/B of the one-fence-per-CTA release: 1 every thread fences (SC), 2 thread 0 SC
     T negz;  // -0 (runtime value for the packed exact products)
     const Ctrl* ctrl;
 };
@@ -1055,10 +1059,13 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
         // release: the CTA's halo stores (ordered before thread 0 by the
         // barrier, fence cumulativity) are made visible system-wide by one
         // fence; the last boundary CTA of the step publishes the next epoch
-        if (a.fence_all) __threadfence_system();
+        if (a.fence_all == 1) __threadfence_system();
         __syncthreads();
         if (tid == 0) {
-            __threadfence_system();
+            if (a.fence_all == 2)
+                __threadfence_system();  // A/B: the sequentially consistent fence of round 2
+            else
+                fence_acq_rel_sys();
             if (a.publish && atomicAdd(&a.peer.self->bnd_done, 1u) == a.n_bnd - 1) {
                 a.peer.self->bnd_done = 0u;
                 peer_publish(a.peer);

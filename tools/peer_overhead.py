@@ -40,7 +40,7 @@ def main():
     stream = torch.cuda.Stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     variants = {"single": {}, "single_same_medium": {}, "peer_middle_rank": {}, "peer_no_segrot": {"FDW_DBG_NO_SEGROT": "1"},
-                "peer_fence_all": {"FDW_DBG_FENCE_ALL": "1"}, "peer_no_halo_store": {"FDW_DBG_NO_HALO_STORE": "1"},
+                "peer_fence_all": {"FDW_DBG_FENCE_ALL": "1"}, "peer_fence_sc": {"FDW_DBG_FENCE_SC": "1"}, "peer_no_halo_store": {"FDW_DBG_NO_HALO_STORE": "1"},
                 "peer_no_pdl": {"FDW_NO_PDL": "1"}}
     only = os.environ.get("CASES")
     res = {k: [] for k in variants if not only or k in only.split(",") or k.startswith("single")}
