@@ -38,6 +38,25 @@ while done < n:
     e1.synchronize()
     out.append(round(e0.elapsed_time(e1) / k * 1000.0, 1))
     done += k
-prof = s.profile_steps(20)
+# FORWARDS more whole forwards first (bench.py runs 3 + 5 before its profile)
+for _ in range(int(os.environ.get("FORWARDS", "0"))):
+    s.reset_state()
+    s.refresh_boundary()
+    s.advance_raw(n, record=True)
+torch.cuda.synchronize()
+# after the run: per-launch profiles of different lengths, interleaved with
+# graph-captured chunks, all from the developed state
+after = []
+for kind, m in (("profile", 20), ("chunk", 100), ("profile", 200), ("chunk", 100), ("profile", 20), ("chunk", 100)):
+    if kind == "profile":
+        after.append([kind, m, round(s.profile_steps(m)[0] * 1000.0, 1)])
+    else:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        s.advance_raw(m, record=True)
+        e1.record(st)
+        e1.synchronize()
+        after.append([kind, m, round(e0.elapsed_time(e1) / m * 1000.0, 1)])
 print(json.dumps({"workload": os.environ.get("WL", "C4"), "chunk": CHUNK, "us_per_step": out,
-                  "mean_us": round(sum(out) / len(out), 1), "profile_developed_ms": [round(x, 5) for x in prof]}))
+                  "mean_us": round(sum(out) / len(out), 1),
+                  "after_run_us": after}))
