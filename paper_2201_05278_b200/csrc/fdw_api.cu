@@ -289,15 +289,20 @@ fdw_status fail(fdw_solver* c, fdw_status s, const char* fmt, ...) {
 
 unsigned long long align_up(unsigned long long v, unsigned long long a) { return (v + a - 1) / a * a; }
 
-// cudaFuncAttributeMaxDynamicSharedMemorySize is per function and process
-// wide: contexts on different host threads share it.  It is only ever raised
-// (a larger limit does not change occupancy), under one lock, so no thread can
-// lower it between another thread's set and launch.
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per function and shared by
+// every context of the process on a device: contexts on different host
+// threads share it.  It is only ever raised (a larger limit does not change
+// occupancy), under one lock, so no thread can lower it between another
+// thread's set and launch.  Tracked per (device, function): the attribute is
+// applied to the function as loaded on the current device, and one process
+// may drive several GPUs (fdw_peer_link, FDW_DEVICES).
 cudaError_t raise_smem_limit(const void* f, size_t bytes) {
     static std::mutex mu;
-    static std::map<const void*, size_t> cur;
+    static std::map<std::pair<int, const void*>, size_t> cur;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
     std::lock_guard<std::mutex> lk(mu);
-    size_t& have = cur[f];
+    size_t& have = cur[{dev, f}];
     if (bytes <= have) return cudaSuccess;
     const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e == cudaSuccess) have = bytes;
