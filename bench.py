@@ -369,19 +369,23 @@ def bench_rank(args, env):
     world, rank, dev = env.world, env.rank, env.device
     wname, cfg = workload_cfg(args.workload, world)
     math_mode = FDW_MATH_EXACT if args.math == "exact" else FDW_MATH_FMA
-    parity = parity_check(env, math_mode) if world > 1 and not args.no_parity else None
+    # 2D does not shard (775k points take ~5 us per step, a
+    # split would be latency-dominated): N GPUs run N independent replicas
+    replicas = world > 1 and cfg.ndim == 2
+    parity = parity_check(env, math_mode) if world > 1 and not replicas and not args.no_parity else None
 
     t0 = time.time()
-    w = build_workload(cfg, np.float32, rank=rank, world=world)
+    w = build_workload(cfg, np.float32, rank=0 if replicas else rank, world=1 if replicas else world)
     setup_s = time.time() - t0
-    slab = w.slab if world > 1 else None
+    slab = w.slab if world > 1 and not replicas else None
     stream = torch.cuda.Stream(device=dev)
 
     def make_solver(vel, eta, mats=None):
         s = Solver(w.grid, mats or make_material_model(vel), DampingField(eta=eta), w.spec, w.axis, w.coeffs,
                    device=dev, math=math_mode, slab=slab)
         s.set_stream(stream.cuda_stream)
-        env.link(s)
+        if not replicas:
+            env.link(s)
         s.set_sources(w.sources, w.wavelet)
         s.set_receivers(w.receivers)
         return s
@@ -389,7 +393,7 @@ def bench_rank(args, env):
     solver = make_solver(w.velocity, w.eta)
     n_steps = w.axis.n_steps
     local_pts = int(np.prod([solver._shape[0] - 2 * w.grid.halo] + list(w.grid.extended_shape[1:w.grid.ndim])))
-    total_pts = w.grid.extended_points()
+    total_pts = w.grid.extended_points() * (world if replicas else 1)
 
     def one_forward():
         solver.reset_state()
@@ -554,7 +558,8 @@ def bench_rank(args, env):
             "space_order": cfg.space_order, "time_steps": n_steps, "points_per_gpu": local_pts,
             "total_points": total_pts, "receivers": w.receivers.n_points, "sources": w.sources.n_points,
             "math": args.math,
-            "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"independent replicas x{world} (2D does not shard)" if replicas else
+                            f"z-slab x{world}" if world > 1 else "single GPU"),
             "step": "one full forward propagation from rest (inject + record every time step, health every 100)",
             "l2": (f"working set {work_bytes / 2**20:.0f} MiB fits the {l2_bytes / 2**20:.0f} MiB L2: L2 flushed "
                    f"({2 * l2_bytes / 2**20:.0f} MiB write) before every timed forward, outside its events"
@@ -579,7 +584,7 @@ def bench_rank(args, env):
         "clocks": clk.summary(),
     }
     if world > 1:
-        line["transport"] = env.transport
+        line["transport"] = "none: independent replicas" if replicas else env.transport
         line["parity"] = parity
     return line
 
