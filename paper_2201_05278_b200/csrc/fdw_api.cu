@@ -775,9 +775,10 @@ bool res2d_configure(fdw_solver* c) {
             }
             if ((long long)zbn * xb > (long long)got * c->sm_count) continue;
             const size_t hb = 2 * c->level_elems * sizeof(T);
-            if (cudaMalloc(&c->d_res_hbuf, hb) != cudaSuccess || cudaMemset(c->d_res_hbuf, 0, hb) != cudaSuccess) {
+            if (cudaMallocAsync(&c->d_res_hbuf, hb, c->stream) != cudaSuccess ||
+                cudaMemsetAsync(c->d_res_hbuf, 0, hb, c->stream) != cudaSuccess) {
                 cudaGetLastError();
-                if (c->d_res_hbuf) cudaFree(c->d_res_hbuf);
+                if (c->d_res_hbuf) cudaFreeAsync(c->d_res_hbuf, c->stream);
                 c->d_res_hbuf = nullptr;
                 break;  // the one-step kernel below
             }
@@ -2482,7 +2483,7 @@ fdw_status fdw_destroy(fdw_solver* c) {
     for (void* p : {(void*)c->d_blk_toff, (void*)c->d_blk_tgt, (void*)c->d_blk_tpos, (void*)c->d_blk_roff,
                     (void*)c->d_blk_rpack, (void*)c->d_tap_ix, c->d_tapbuf})
         if (p) cudaFreeAsync(p, c->stream);
-    if (c->d_res_hbuf) cudaFree(c->d_res_hbuf);
+    if (c->d_res_hbuf) cudaFreeAsync(c->d_res_hbuf, c->stream);
     for (void* p : {(void*)c->d_sp_idx, (void*)c->d_sp_w, (void*)c->d_sp_prod})
         if (p) cudaFreeAsync(p, c->stream);
     for (void* p : {(void*)c->d_eidx, (void*)c->d_etab})
@@ -3105,14 +3106,17 @@ fdw_status fdw_download_seismogram(fdw_solver* c, void* out, uint64_t rows) {
     if (s) return s;
     if (rows > c->seis_rows) return fail(c, FDW_EINVAL, "rows exceed the seismogram");
     const size_t n = (size_t)rows * c->n_rec;
-    std::vector<double> tmp(n);
-    if ((s = fdw_download_seismogram_f64(c, tmp.data(), rows))) return s;
-    if (c->tsize == 4) {
-        float* o = static_cast<float*>(out);
-        for (size_t i = 0; i < n; ++i) o[i] = static_cast<float>(tmp[i]);
-    } else {
-        std::memcpy(out, tmp.data(), n * sizeof(double));
-    }
+    if (c->tsize == 8 || n == 0) return fdw_download_seismogram_f64(c, static_cast<double*>(out), rows);
+    // fp32: rows rounded on the device, one D2H copy straight into `out`
+    float* tmp = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * sizeof(float), c->stream));
+    const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)c->sm_count * 8);
+    fdw::seis_to_float<<<blocks, 256, 0, c->stream>>>(c->d_seis, tmp, (unsigned long long)n);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, tmp, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream);
+    cudaFreeAsync(tmp, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return fail(c, FDW_ECUDA, "fdw_download_seismogram: %s", cudaGetErrorString(e));
     return FDW_OK;
 }
 

@@ -2773,6 +2773,14 @@ __global__ void box_copy(T* __restrict__ dst, long long d_plane, long long d_row
     }
 }
 
+// Seismogram rows to T (Seismogram<T> holds T(sum), acquisition.hpp:158):
+// double -> float rounds to nearest, as static_cast<float> does on the host.
+__global__ void seis_to_float(const double* __restrict__ in, float* __restrict__ out, unsigned long long n) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        out[i] = __double2float_rn(in[i]);
+}
+
 template <typename T>
 __global__ void c2dt2_kernel(T* f, unsigned long long n, double dt) {
     const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
