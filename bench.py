@@ -68,6 +68,17 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def replicated(cfg, world):
+    """2D does not shard: N GPUs run N independent replicas."""
+    return world > 1 and cfg.ndim == 2
+
+
+def l2_flush_needed(points, l2_bytes):
+    """Timing rule: inputs larger than L2, or L2 flushed between timed steps.
+    The working set is 4 fp32 fields (two levels, c2dt2, damping) of `points`."""
+    return 4 * points * 4 < 2 * l2_bytes
+
+
 def workload_cfg(name, world):
     """auto: C4 on one GPU, C5 (weak scaling, 200 planes per GPU) on N > 1.
     C3 / C4 on N > 1 are strong scaling (the one grid split into N slabs);
@@ -371,7 +382,7 @@ def bench_rank(args, env):
     math_mode = FDW_MATH_EXACT if args.math == "exact" else FDW_MATH_FMA
     # 2D does not shard (775k points take ~5 us per step, a
     # split would be latency-dominated): N GPUs run N independent replicas
-    replicas = world > 1 and cfg.ndim == 2
+    replicas = replicated(cfg, world)
     parity = parity_check(env, math_mode) if world > 1 and not replicas and not args.no_parity else None
 
     t0 = time.time()
@@ -411,7 +422,7 @@ def bench_rank(args, env):
     # stays outside the timed region).
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     work_bytes = 4 * local_pts * 4
-    flush = work_bytes < 2 * l2_bytes
+    flush = l2_flush_needed(local_pts, l2_bytes)
     scrub = torch.empty(2 * l2_bytes // 4 + 1024, dtype=torch.float32, device=dev) if flush else None
     l0 = solver.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
