@@ -3107,6 +3107,7 @@ fdw_status fdw_download_seismogram(fdw_solver* c, void* out, uint64_t rows) {
     if (rows > c->seis_rows) return fail(c, FDW_EINVAL, "rows exceed the seismogram");
     const size_t n = (size_t)rows * c->n_rec;
     if (c->tsize == 8 || n == 0) return fdw_download_seismogram_f64(c, static_cast<double*>(out), rows);
+    if (!c->d_seis) return fail(c, FDW_ESTATE, "no seismogram: set_receivers first");
     // fp32: rows rounded on the device, one D2H copy straight into `out`
     float* tmp = nullptr;
     CU(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * sizeof(float), c->stream));
