@@ -146,19 +146,31 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+SWEEP_END_MARKER = "// 2D: one persistent cooperative kernel runs a whole chunk"
+
+
+def sweep_source_sha():
+    """SHA-256 of fdw_kernels.cuh up to the end of the 3D TMA sweep: the sweep
+    and everything it can use is defined before the 2D section, so edits
+    further down (2D kernels, small helpers) do not invalidate a capture."""
+    import hashlib
+    with open(os.path.join(ROOT, "paper_2201_05278_b200", "csrc", "fdw_kernels.cuh"), "rb") as f:
+        src = f.read()
+    end = src.find(SWEEP_END_MARKER.encode())
+    return hashlib.sha256(src if end < 0 else src[:end]).hexdigest()
+
+
 def traffic_for(workload):
     """DRAM bytes (read + write) per sweep launch from the committed ncu capture
     (profiles/ncu_traffic.json).  Valid only for the kernel source it was
-    captured from: the capture records the SHA-256 of csrc/fdw_kernels.cuh, and
-    a changed source reports null instead of a stale number."""
-    import hashlib
+    captured from: the capture records the SHA-256 of the sweep's source
+    (sweep_source_sha), and a changed sweep reports null instead of a stale
+    number."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
-        with open(os.path.join(ROOT, "paper_2201_05278_b200", "csrc", "fdw_kernels.cuh"), "rb") as f:
-            cur = hashlib.sha256(f.read()).hexdigest()
-        if d.get("kernels_sha256") != cur:
-            return None, "stale: fdw_kernels.cuh changed since the ncu capture"
+        if d.get("sweep_source_sha256") != sweep_source_sha():
+            return None, "stale: the sweep's source changed since the ncu capture"
         return d.get(workload), d.get("source")
     except Exception as e:
         return None, f"unavailable: {e}"
