@@ -2415,15 +2415,17 @@ fdw_status fdw_create(const fdw_desc* dp, fdw_solver** out) {
                 minb = (cudaFuncGetAttributes(&fa, f3) == cudaSuccess && fa.localSizeBytes <= 8) ? 3 : 2;
             }
             c->tma_minb = minb;
-            // split rings (2 planes in flight at 3 CTAs/SM; float): the default;
+            // split rings (2 planes in flight at 3 CTAs/SM): the default;
             // FDW_TMA_PD=0 restores the single ring (developed C4 field, same box:
-            // sweep 528.6 -> 517.8 us, step 518.4 -> 516.7 us, profiles/r02/ab_pd.json)
+            // sweep 528.6 -> 517.8 us, step 518.4 -> 516.7 us, profiles/r02/ab_pd.json;
+            // fp64 C4 from rest: 1.043 -> 1.024 ms/step, 72 KB at 3 CTAs/SM)
             const char* pde = std::getenv("FDW_TMA_PD");
             const bool split = pde ? std::atoi(pde) > 0 : true;
-            c->tma_pd = (split && c->tsize == 4 && minb == 3) ? TMA_PD : 0;
+            c->tma_pd = (split && minb == 3) ? TMA_PD : 0;
             const void* f = c->tsize == 4 ? tma_kernel<float>(R, ex, minb, c->tma_pd)
-                                          : tma_kernel<double>(R, ex, minb);
-            const int smem = c->tsize == 4 ? tma_smem<float>(R, false, c->tma_pd) : tma_smem<double>(R);
+                                          : tma_kernel<double>(R, ex, minb, c->tma_pd);
+            const int smem = c->tsize == 4 ? tma_smem<float>(R, false, c->tma_pd)
+                                           : tma_smem<double>(R, false, c->tma_pd);
             if (!ck(raise_smem_limit(f, smem), "smem attr"))
                 return bail(FDW_ECUDA);
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 16 * TMA_BX, smem) != cudaSuccess || occ < 1)

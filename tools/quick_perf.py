@@ -6,11 +6,11 @@ from paper_2201_05278_b200 import configs, Solver, make_material_model, DampingF
 from paper_2201_05278_b200._lib import *
 
 _cache = {}
-def run(name, cfg, steps, density=False, **kw):
-    key = cfg.name
+def run(name, cfg, steps, density=False, dtype=np.float32, **kw):
+    key = (cfg.name, np.dtype(dtype).str)
     if key not in _cache:
         _cache.clear()
-        _cache[key] = configs.build_workload(cfg, np.float32)
+        _cache[key] = configs.build_workload(cfg, dtype)
     w = _cache[key]
     rho = None
     if density:  # layered density (g/cm^3) following the velocity, Gardner-like
@@ -23,7 +23,7 @@ def run(name, cfg, steps, density=False, **kw):
     ms = s.profile_steps(20)
     out = dict(name=name, kw={k: int(v) for k, v in kw.items()}, layout=s.layout(),
                gpts=round(pts * steps / el / 1e9, 2), ms_step=round(el / steps * 1e3, 4), prof_ms=[round(x, 4) for x in ms],
-               sweep_gbs=round(pts * 20 / (ms[0] * 1e-3) / 1e9, 1))
+               sweep_gbs=round(pts * 5 * np.dtype(dtype).itemsize / (ms[0] * 1e-3) / 1e9, 1))
     print(json.dumps(out), flush=True)
     s.close()
 
@@ -40,6 +40,11 @@ if __name__ == "__main__":
     if "c4only" in which:
         run("C4-tma", c4, 400)
         run("C4-tma-fma", c4, 400, math=FDW_MATH_FMA)
+        sys.exit(0)
+    if "f64" in which:
+        run("C4-f64", c4, 400, dtype=np.float64)
+        run("C4-f32", c4, 400)
+        run("C2-f64", configs.marmousi2d(8), 1600, dtype=np.float64)
         sys.exit(0)
     if "vd" in which:
         run("C4-vd", c4, 200, density=True)
