@@ -166,7 +166,7 @@ struct fdw_solver {
     int tma_pd = 0;  // > 0: split-ring TMA sweep with that many planes in flight
     // damping table (split-ring fp32 sweep): 1-byte eta index per point, (om, iop) per index
     unsigned char* d_eidx = nullptr;
-    float2* d_etab = nullptr;
+    void* d_etab = nullptr;  // float2 / double2 pairs
     int n_etab = 0;          // entries incl. index 0; 0: no table (the sweep streams fp32 eta)
     CUtensorMap tm_eb{};     // TMA map over d_eidx
 
@@ -470,7 +470,7 @@ SweepArgs<T> sweep_args(fdw_solver* c, int src, int dst) {
     a.ctrl = c->ctrl;
     a.ezr = c->d_ezr;
     a.seg_rot = 0;
-    a.etab = c->d_etab;
+    a.etab = static_cast<const typename fdw::EtabPair<T>::type*>(c->d_etab);
     a.n_etab = c->n_etab;
     a.negz = static_cast<T>(-0.0);
     if (c->vd) {
@@ -604,7 +604,8 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
         a.fence_all = c->dbg_fence_all ? 1 : c->dbg_fence_sc ? 2 : 0;
     }
     const int col_base = (int)(c->base + c->R);
-    const bool etab = c->tma_pd > 0 && c->n_etab > 0;
+    // the damping table: fp32 and fp64 constant density, fp32 density
+    const bool etab = c->tma_pd > 0 && c->n_etab > 0 && (!c->vd || std::is_same<T, float>::value);
     // density: split rings only together with the damping table (vd_fast)
     const int pd = c->vd ? (etab ? c->tma_pd : 0) : c->tma_pd;
     const int smem = tma_smem<T>(c->R, c->vd, pd);
@@ -633,13 +634,10 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
     cfg.attrs = attr;
     cfg.numAttrs = na;
     if (c->R != 1 && c->R != 2 && c->R != 4) return false;
-    constexpr bool F32 = std::is_same<T, float>::value;
     const void* kern = nullptr;
     if (c->vd) {
-        if (etab && !F32) return false;
         kern = tma_vd_kernel<T>(c->R, EX, etab);
     } else if (pd > 0) {
-        if (etab && !F32) return false;
         kern = tma_kernel<T>(c->R, EX, 3, pd, etab);
     } else {
         kern = tma_kernel<T>(c->R, EX, c->tma_minb == 3 ? 3 : 2);
@@ -2523,63 +2521,80 @@ fdw_status fdw_set_stream(fdw_solver* c, void* stream) {
 // order, (1 - eta dt, 1/(1 + eta dt)) formed in double exactly as
 // kernel.hpp:284-287, then a 1-byte index per point.  More than 255 distinct
 // values: no table (the sweep streams fp32 eta as before).
-static fdw_status build_eta_table(fdw_solver* c) {
-    c->n_etab = 0;
-    if (std::getenv("FDW_NO_ETAB") || c->tsize != 4 || c->variant != FDW_KERNEL_TMA || c->tma_pd == 0) return FDW_OK;
+extern "C++" {
+template <typename T>
+fdw_status build_eta_table_t(fdw_solver* c) {
+    using K = std::conditional_t<sizeof(T) == 4, unsigned, unsigned long long>;
+    using T2 = typename fdw::EtabPair<T>::type;
+    const K EMPTY = ~K(0);
     const unsigned long long n = c->level_elems;
-    unsigned* keys = nullptr;
-    CU(cudaMallocAsync(reinterpret_cast<void**>(&keys), (fdw::ETAB_CAP + 1) * sizeof(unsigned), c->stream));
-    CU(cudaMemsetAsync(keys, 0xFF, fdw::ETAB_CAP * sizeof(unsigned), c->stream));
-    CU(cudaMemsetAsync(keys + fdw::ETAB_CAP, 0, sizeof(unsigned), c->stream));
-    fdw::eta_collect<<<c->sm_count * 8, 256, 0, c->stream>>>(static_cast<const float*>(c->eta), n, keys,
-                                                              keys + fdw::ETAB_CAP);
+    K* keys = nullptr;
+    unsigned* overflow = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&keys), fdw::ETAB_CAP * sizeof(K) + sizeof(unsigned), c->stream));
+    overflow = reinterpret_cast<unsigned*>(keys + fdw::ETAB_CAP);
+    CU(cudaMemsetAsync(keys, 0xFF, fdw::ETAB_CAP * sizeof(K), c->stream));
+    CU(cudaMemsetAsync(overflow, 0, sizeof(unsigned), c->stream));
+    fdw::eta_collect<T><<<c->sm_count * 8, 256, 0, c->stream>>>(static_cast<const T*>(c->eta), n, keys, overflow);
     CHECK_LAUNCH();
-    std::vector<unsigned> h(fdw::ETAB_CAP + 1);
-    CU(cudaMemcpyAsync(h.data(), keys, h.size() * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+    std::vector<K> h(fdw::ETAB_CAP);
+    unsigned ovf = 0;
+    CU(cudaMemcpyAsync(h.data(), keys, h.size() * sizeof(K), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(&ovf, overflow, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
-    std::vector<float> vals;
+    std::vector<T> vals;
     for (int k = 0; k < fdw::ETAB_CAP; ++k)
-        if (h[k] != fdw::ETAB_EMPTY) {
-            float f;
-            std::memcpy(&f, &h[k], 4);
+        if (h[k] != EMPTY) {
+            T f;
+            std::memcpy(&f, &h[k], sizeof(T));
             vals.push_back(f);
         }
-    if (h[fdw::ETAB_CAP] || vals.size() > 255) {
+    if (ovf || vals.size() > 255) {
         cudaFreeAsync(keys, c->stream);
         return FDW_OK;
     }
     std::sort(vals.begin(), vals.end());
-    std::vector<float2> tab(256, make_float2(1.0f, 1.0f));
+    std::vector<T2> tab(256);
+    tab[0].x = T(1);
+    tab[0].y = T(1);
     std::vector<unsigned char> slot(fdw::ETAB_CAP, 0);
     for (size_t i = 0; i < vals.size(); ++i) {
         volatile double edt = static_cast<double>(vals[i]) * c->d.dt;  // no contraction: as damping_factors
         const double e = edt;
-        tab[i + 1] = make_float2(static_cast<float>(1.0 - e), static_cast<float>(1.0 / (1.0 + e)));
-        unsigned bits;
-        std::memcpy(&bits, &vals[i], 4);
+        tab[i + 1].x = static_cast<T>(1.0 - e);
+        tab[i + 1].y = static_cast<T>(1.0 / (1.0 + e));
+        K bits;
+        std::memcpy(&bits, &vals[i], sizeof(T));
         for (int k = 0; k < fdw::ETAB_CAP; ++k)
             if (h[k] == bits) slot[k] = static_cast<unsigned char>(i + 1);
     }
     unsigned char* d_slot = nullptr;
     CU(cudaMallocAsync(reinterpret_cast<void**>(&d_slot), fdw::ETAB_CAP, c->stream));
     CU(cudaMemcpyAsync(d_slot, slot.data(), fdw::ETAB_CAP, cudaMemcpyHostToDevice, c->stream));
-    if (!c->d_etab) CU(cudaMallocAsync(reinterpret_cast<void**>(&c->d_etab), 256 * sizeof(float2), c->stream));
-    CU(cudaMemcpyAsync(c->d_etab, tab.data(), 256 * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
+    if (!c->d_etab) CU(cudaMallocAsync(&c->d_etab, 256 * sizeof(T2), c->stream));
+    CU(cudaMemcpyAsync(c->d_etab, tab.data(), 256 * sizeof(T2), cudaMemcpyHostToDevice, c->stream));
     if (!c->d_eidx) CU(cudaMallocAsync(reinterpret_cast<void**>(&c->d_eidx), n, c->stream));
-    fdw::eta_index<<<c->sm_count * 8, 256, 0, c->stream>>>(static_cast<const float*>(c->eta), n, keys, d_slot,
-                                                            c->d_eidx);
+    fdw::eta_index<T><<<c->sm_count * 8, 256, 0, c->stream>>>(static_cast<const T*>(c->eta), n, keys, d_slot,
+                                                               c->d_eidx);
     CHECK_LAUNCH();
     cudaFreeAsync(keys, c->stream);
     cudaFreeAsync(d_slot, c->stream);
-    if (!make_map(c, &c->tm_eb, c->d_eidx, fdw::TmaShape<float, 1, TMA_BX>::TYW, TMA_BX,
+    // the index tile has the sweep's tile shape (TYW x BX points), 1 byte each
+    if (!make_map(c, &c->tm_eb, c->d_eidx, fdw::TmaShape<T, 1, TMA_BX>::TYW, TMA_BX,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, 1))
         return fail(c, FDW_ECUDA, "cuTensorMapEncodeTiled failed (eta index map)");
     const bool ex = c->d.math == FDW_MATH_EXACT;
-    const void* f = tma_kernel<float>(c->R, ex, 3, c->tma_pd, true);
+    const void* f = tma_kernel<T>(c->R, ex, 3, c->tma_pd, true);
     if (!f) return FDW_OK;
-    CU(raise_smem_limit(f, tma_smem<float>(c->R, false, c->tma_pd)));
+    CU(raise_smem_limit(f, tma_smem<T>(c->R, false, c->tma_pd)));
     c->n_etab = (int)vals.size() + 1;
     return FDW_OK;
+}
+}  // extern "C++"
+
+static fdw_status build_eta_table(fdw_solver* c) {
+    c->n_etab = 0;
+    if (std::getenv("FDW_NO_ETAB") || c->variant != FDW_KERNEL_TMA || c->tma_pd == 0) return FDW_OK;
+    return c->tsize == 4 ? build_eta_table_t<float>(c) : build_eta_table_t<double>(c);
 }
 
 fdw_status fdw_set_medium(fdw_solver* c, const void* velocity, const void* eta, int on_device) {

@@ -36,19 +36,15 @@ const void* tma_vd_kernel(int R, bool ex, bool fast) {
 
 template <typename T>
 const void* tma_kernel(int R, bool ex, int minb, int pd, bool etab) {
-    if constexpr (std::is_same<T, float>::value) {
-        if (pd > 0 && etab) {  // split rings with the damping table
+    if (pd > 0 && etab) {  // split rings with the damping table (fp32 and fp64)
 #define TKE(RR) \
     if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 3, false, TMA_PD, true> \
                            : (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, false, 3, false, TMA_PD, true>;
-            TKE(1)
-            TKE(2)
-            TKE(4)
+        TKE(1)
+        TKE(2)
+        TKE(4)
 #undef TKE
-            return nullptr;
-        }
-    } else {
-        if (pd > 0 && etab) return nullptr;
+        return nullptr;
     }
     if (pd > 0) {  // split rings: 3 CTAs/SM only
 #define TKP(RR) \

@@ -239,6 +239,18 @@ __device__ __forceinline__ T time_update(T rhs, T uc, T c2, T prev, T eta, doubl
     return A::mul(A::sub(t, A::mul(om, prev)), iop);
 }
 
+// (1 - eta dt, 1/(1 + eta dt)) pairs of the damping table, in T
+template <typename T>
+struct EtabPair;
+template <>
+struct EtabPair<float> {
+    using type = float2;
+};
+template <>
+struct EtabPair<double> {
+    using type = double2;
+};
+
 template <typename T>
 struct SweepArgs {
     const T* __restrict__ u;      // current level
@@ -262,9 +274,9 @@ struct SweepArgs {
     // TMA sweep: per tile column, the Z range [x, y) of planes whose eta tile
     // is all zero (those planes skip the eta stream); null: none
     const int2* ezr;
-    // split-ring fp32 sweep with a damping table: (1 - eta dt, 1/(1 + eta dt))
-    // per index, index 0 = undamped; the eta map then streams 1-byte indices
-    const float2* etab;
+    // split-ring sweep with a damping table: (1 - eta dt, 1/(1 + eta dt)) per
+    // index, index 0 = undamped; the eta map then streams 1-byte indices
+    const typename EtabPair<T>::type* etab;
     int n_etab;
     // TMA sweep Z segments: CTA z-index b sweeps segment (b + seg_rot) mod
     // gridDim.z; a slab rotates its boundary segments (S-1, 0) into the first
@@ -615,7 +627,9 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
     constexpr int V = S::V, NTY = S::NTY, TYW = S::TYW, HY = S::HY, HYV = HY / V, UW = S::UW, NU = S::NU;
     constexpr int NH = S::NH, NP = S::NP;
     constexpr int THREADS = S::THREADS;
-    static_assert(!ETAB || (std::is_same<T, float>::value && V == 4), "damping table: fp32 only");
+    static_assert(!ETAB || ((std::is_same<T, float>::value && V == 4) || (std::is_same<T, double>::value && V == 2)),
+                  "damping table: fp32 or fp64");
+    using T2 = typename EtabPair<T>::type;
     constexpr int E_BOX = ETAB ? TYW * BX : S::P_BOX;  // bytes of the eta (or eta index) tile
     using VT = Vec<T, V>;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -690,7 +704,7 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
         for (int k = 0; k < NU + NH + NP; ++k) mbar_init(&barU[k], 1);  // barU, barH, barP are contiguous
         mbar_fence_init();
     }
-    __shared__ float2 s_etab[ETAB ? 256 : 1];
+    __shared__ T2 s_etab[ETAB ? 256 : 1];
     if constexpr (ETAB)
         for (int k = tid; k < a.n_etab; k += THREADS) s_etab[k] = a.etab[k];
     __syncthreads();
@@ -977,12 +991,18 @@ __global__ void __launch_bounds__(TmaShape<T, R, BX, VD ? 6 : 3, PD>::THREADS, M
                 for (int e = 0; e < V; ++e)
                     res.e[e] = A::sub(A::add(A::mul(cc.e[e], rhs_of(e)), A::mul(T(2), q[R].e[e])), pc.e[e]);
             } else if constexpr (ETAB) {  // tabled factors; index 0 = (1, 1) is exact
-                const uchar4 ib = *reinterpret_cast<const uchar4*>(
-                    reinterpret_cast<const unsigned char*>(p_stage(it, 2)) + po);
-                const unsigned ix[4] = {ib.x, ib.y, ib.z, ib.w};
+                const unsigned char* ibp = reinterpret_cast<const unsigned char*>(p_stage(it, 2)) + po;
+                unsigned ix[V];
+                if constexpr (V == 4) {
+                    const uchar4 ib = *reinterpret_cast<const uchar4*>(ibp);
+                    ix[0] = ib.x, ix[1] = ib.y, ix[2] = ib.z, ix[3] = ib.w;
+                } else {
+                    const uchar2 ib = *reinterpret_cast<const uchar2*>(ibp);
+                    ix[0] = ib.x, ix[1] = ib.y;
+                }
     #pragma unroll
                 for (int e = 0; e < V; ++e) {
-                    const float2 f = s_etab[ix[e]];
+                    const T2 f = s_etab[ix[e]];
                     const T t = A::add(A::mul(cc.e[e], rhs_of(e)), A::mul(T(2), q[R].e[e]));
                     res.e[e] = A::mul(A::sub(t, A::mul(f.x, pc.e[e])), f.y);
                 }
@@ -2711,26 +2731,44 @@ __global__ void eta_zero_ranges(const T* __restrict__ eta, long long origin, lon
 // exactly as kernel.hpp:284-287 (bit-identical to forming them per point).
 // Pass 1: distinct non-zero bit patterns into an open-addressing set.
 constexpr int ETAB_CAP = 1024;  // set slots (power of two)
-constexpr unsigned ETAB_EMPTY = 0xFFFFFFFFu;
-__device__ __forceinline__ unsigned etab_hash(unsigned v) {
+// Set keys are the bit patterns of T(eta): 32-bit for float, 64-bit for double;
+// the all-ones pattern (a NaN) marks an empty slot.
+template <typename T>
+struct EtaKey;
+template <>
+struct EtaKey<float> {
+    using type = unsigned;
+    static __device__ __forceinline__ type bits(float f) { return __float_as_uint(f); }
+};
+template <>
+struct EtaKey<double> {
+    using type = unsigned long long;
+    static __device__ __forceinline__ type bits(double f) { return (unsigned long long)__double_as_longlong(f); }
+};
+__device__ __forceinline__ unsigned etab_hash(unsigned long long w) {
+    unsigned v = (unsigned)(w ^ (w >> 32));
     v ^= v >> 16;
     v *= 0x7feb352du;
     v ^= v >> 15;
     return v & (ETAB_CAP - 1);
 }
-__global__ void eta_collect(const float* __restrict__ eta, unsigned long long n, unsigned* keys, unsigned* overflow) {
+template <typename T>
+__global__ void eta_collect(const T* __restrict__ eta, unsigned long long n, typename EtaKey<T>::type* keys,
+                            unsigned* overflow) {
+    using K = typename EtaKey<T>::type;
+    constexpr K EMPTY = ~K(0);
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
-        const float f = eta[i];
-        if (f == 0.0f) continue;
-        const unsigned v = __float_as_uint(f);
+        const T f = eta[i];
+        if (f == T(0)) continue;
+        const K v = EtaKey<T>::bits(f);
         unsigned h = etab_hash(v);
         for (int probe = 0;; ++probe) {
-            const unsigned k = *reinterpret_cast<volatile unsigned*>(&keys[h]);
+            const K k = *reinterpret_cast<volatile K*>(&keys[h]);
             if (k == v) break;
-            if (k == ETAB_EMPTY) {
-                const unsigned old = atomicCAS(&keys[h], ETAB_EMPTY, v);
-                if (old == ETAB_EMPTY || old == v) break;
+            if (k == EMPTY) {
+                const K old = atomicCAS(&keys[h], EMPTY, v);
+                if (old == EMPTY || old == v) break;
             }
             if (probe >= ETAB_CAP) {
                 atomicOr(overflow, 1u);
@@ -2741,14 +2779,16 @@ __global__ void eta_collect(const float* __restrict__ eta, unsigned long long n,
     }
 }
 // Pass 2: the index of every point (0: eta == 0, undamped).
-__global__ void eta_index(const float* __restrict__ eta, unsigned long long n, const unsigned* __restrict__ keys,
+template <typename T>
+__global__ void eta_index(const T* __restrict__ eta, unsigned long long n,
+                          const typename EtaKey<T>::type* __restrict__ keys,
                           const unsigned char* __restrict__ slot_index, unsigned char* __restrict__ out) {
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
-        const float f = eta[i];
+        const T f = eta[i];
         unsigned char ix = 0;
-        if (f != 0.0f) {
-            const unsigned v = __float_as_uint(f);
+        if (f != T(0)) {
+            const typename EtaKey<T>::type v = EtaKey<T>::bits(f);
             unsigned h = etab_hash(v);
             while (keys[h] != v) h = (h + 1) & (ETAB_CAP - 1);
             ix = slot_index[h];

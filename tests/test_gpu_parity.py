@@ -174,15 +174,16 @@ def test_verbose_progress_line(capsys):
 
 
 @pytest.mark.parametrize("n_distinct", [7, 255, 256, 5000])
-def test_damping_table_and_fallback(n_distinct):
-    """The fp32 TMA sweep streams a 1-byte damping index with a (1 - eta dt,
-    1/(1 + eta dt)) table when eta has <= 255 distinct non-zero values, and the
-    fp32 eta otherwise: both bit-exact against the oracle, on an eta field
-    with arbitrary values everywhere (not just an absorbing shell)."""
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_damping_table_and_fallback(n_distinct, dtype):
+    """The TMA sweep (fp32 and fp64) streams a 1-byte damping index with a
+    (1 - eta dt, 1/(1 + eta dt)) table when eta has <= 255 distinct non-zero
+    values, and T(eta) otherwise: both bit-exact against the oracle, on an eta
+    field with arbitrary values everywhere (not just an absorbing shell)."""
     cfg = small_config(ndim=3, order=8, shape=(23, 27, 70), steps=40, n_rec=8)
-    w = build_workload(cfg, np.float32)
+    w = build_workload(cfg, dtype)
     rng = np.random.default_rng(n_distinct)
-    values = rng.uniform(1.0, 60.0, n_distinct).astype(np.float32)
+    values = rng.uniform(1.0, 60.0, n_distinct).astype(dtype)
     eta = values[rng.integers(0, n_distinct, w.eta.shape)]
     eta[rng.random(w.eta.shape) < 0.5] = 0.0  # undamped points interleaved
     w.eta = np.ascontiguousarray(eta)
