@@ -604,8 +604,7 @@ bool launch_tma(fdw_solver* c, const SweepArgs<T>& a0, int src, int dst) {
         a.fence_all = c->dbg_fence_all ? 1 : c->dbg_fence_sc ? 2 : 0;
     }
     const int col_base = (int)(c->base + c->R);
-    // the damping table: fp32 and fp64 constant density, fp32 density
-    const bool etab = c->tma_pd > 0 && c->n_etab > 0 && (!c->vd || std::is_same<T, float>::value);
+    const bool etab = c->tma_pd > 0 && c->n_etab > 0;
     // density: split rings only together with the damping table (vd_fast)
     const int pd = c->vd ? (etab ? c->tma_pd : 0) : c->tma_pd;
     const int smem = tma_smem<T>(c->R, c->vd, pd);
@@ -2666,12 +2665,19 @@ fdw_status fdw_set_density(fdw_solver* c, const void* rho, int on_device) {
             if (!make_map(c, &c->tm_g[ax], c->grad[ax], pw, TMA_BX))
                 return fail(c, FDW_ECUDA, "cuTensorMapEncodeTiled failed (density maps)");
         const bool ex = c->d.math == FDW_MATH_EXACT;
-        const bool fast = c->tsize == 4 && c->tma_pd > 0 && c->n_etab > 0;  // as launch_tma chooses
-        const void* f = c->tsize == 4 ? tma_vd_kernel<float>(c->R, ex, fast) : tma_vd_kernel<double>(c->R, ex);
-        const int smem = c->tsize == 4 ? tma_smem<float>(c->R, true, fast ? TMA_PD : 0) : tma_smem<double>(c->R, true);
-        CU(raise_smem_limit(f, smem));
-        if (fast)  // a later set_medium may drop the table: keep the single-ring kernel launchable
-            CU(raise_smem_limit(tma_vd_kernel<float>(c->R, ex), tma_smem<float>(c->R, true)));
+        const bool fast = c->tma_pd > 0 && c->n_etab > 0;  // as launch_tma chooses
+        auto vd_fn = [&](bool fst) {
+            return c->tsize == 4 ? tma_vd_kernel<float>(c->R, ex, fst) : tma_vd_kernel<double>(c->R, ex, fst);
+        };
+        auto vd_smem = [&](bool fst) {
+            return c->tsize == 4 ? tma_smem<float>(c->R, true, fst ? TMA_PD : 0)
+                                 : tma_smem<double>(c->R, true, fst ? TMA_PD : 0);
+        };
+        const void* f = vd_fn(fast);
+        const int smem = vd_smem(fast);
+        // both variants stay launchable: a later set_medium may build or drop the table
+        CU(raise_smem_limit(vd_fn(false), vd_smem(false)));
+        if (c->tma_pd > 0) CU(raise_smem_limit(vd_fn(true), vd_smem(true)));
         int occ = 1;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 16 * TMA_BX, smem) != cudaSuccess || occ < 1)
             occ = 1;

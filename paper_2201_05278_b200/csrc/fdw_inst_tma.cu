@@ -12,17 +12,15 @@ namespace fdwi {
 
 template <typename T>
 const void* tma_vd_kernel(int R, bool ex, bool fast) {
-    if constexpr (std::is_same<T, float>::value) {
-        if (fast) {  // split rings + damping table
+    if (fast) {  // split rings + damping table (fp32 and fp64)
 #define TKVF(RR) \
     if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 2, true, TMA_PD, true> \
                            : (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, false, 2, true, TMA_PD, true>;
-            TKVF(1)
-            TKVF(2)
-            TKVF(4)
+        TKVF(1)
+        TKVF(2)
+        TKVF(4)
 #undef TKVF
-            return nullptr;
-        }
+        return nullptr;
     }
 #define TKV(RR) \
     if (R == RR) return ex ? (const void*)fdw::sweep3d_tma<T, RR, TMA_BX, true, 2, true> \

@@ -14,7 +14,7 @@ def run(name, cfg, steps, density=False, dtype=np.float32, **kw):
     w = _cache[key]
     rho = None
     if density:  # layered density (g/cm^3) following the velocity, Gardner-like
-        rho = (0.31 * np.power(w.velocity.astype(np.float64), 0.25)).astype(np.float32)
+        rho = (0.31 * np.power(w.velocity.astype(np.float64), 0.25)).astype(w.velocity.dtype)
     s = Solver(w.grid, make_material_model(w.velocity, rho), DampingField(eta=w.eta), w.spec, w.axis, w.coeffs, **kw)
     s.set_sources(w.sources, w.wavelet); s.set_receivers(w.receivers)
     s.advance_raw(100, record=True)  # warm (graph capture)
@@ -45,6 +45,7 @@ if __name__ == "__main__":
         run("C4-f64", c4, 400, dtype=np.float64)
         run("C4-f32", c4, 400)
         run("C2-f64", configs.marmousi2d(8), 1600, dtype=np.float64)
+        run("C4-vd-f64", c4, 200, density=True, dtype=np.float64)
         sys.exit(0)
     if "vd" in which:
         run("C4-vd", c4, 200, density=True)
